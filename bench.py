@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Throughput bench of the B200 tactile path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (N=1): BASELINE configs[2] -- 4096 envs of 240x320 synthetic height
+maps (sphere / cylinder / cube edge / Perlin plate, penetration U(0, 1.2 mm)),
+sigma (1,2,4) pyramid, 125x180 random LUT, U[80,160] background, 7x9
+markers with random shear/twist, dots r=3.  One step = one fused
+``tac_pipeline`` launch over all envs.  N>1: every rank runs its own 4096-env
+block (weak scaling; at N=8 that is configs[4]'s 32768 envs) plus the NCCL
+all-gather of the [N, 8] contact summaries once per step.
+
+Prints ONE JSON line (rank 0).
+"""
+
+import argparse
+import json
+import math
+import multiprocessing as mproc
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tactile frames/s (RGB+markers)"
+UNIT = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[i] (1, 2 or 3)")
+    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- CPU arm
+def _cpu_worker(args):
+    """Time the oracle port on a slice of frames (one single-threaded process)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cfg_index, seed, start, count = args
+    import torch
+
+    torch.set_num_threads(1)
+    from oracle.fast import FastOracle
+    from paper_2411_04776_b200 import synthetic
+
+    cfg, _ = synthetic.baseline_config(cfg_index, seed)
+    h, w = cfg.sensor.image_size
+    p = synthetic.indenters(start + count, h, w, seed + 10)
+    sel = synthetic.IndenterParams(*(getattr(p, f)[start:] for f in
+                                     ("kind", "pen", "cx", "cy", "yaw", "perm", "off")))
+    depth = synthetic.height_maps(sel, h, w, dtype=torch.float64).numpy()
+    shear, twist = synthetic.loads(start + count, seed + 20)
+    orc = FastOracle(cfg)
+    orc.run(depth[0], shear[start], twist[start])  # warm
+    t0 = time.perf_counter()
+    for i in range(count):
+        orc.run(depth[i], shear[start + i], twist[start + i])
+    return count, time.perf_counter() - t0
+
+
+def cpu_rate(cfg_index, seed, cores, frames_per_core):
+    """Aggregate frames/s of the oracle port on `cores` processes."""
+    jobs = [(cfg_index, seed, i * frames_per_core, frames_per_core) for i in range(cores)]
+    ctx = mproc.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    frames = sum(r[0] for r in res)
+    per_core = statistics.mean(r[0] / r[1] for r in res)
+    return frames, per_core * cores, per_core, wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def calibrate_frames_per_core(cfg_index, seed, seconds):
+    """Frames per core so the pool spends ~`seconds` of wall time."""
+    n, dt = _cpu_worker((cfg_index, seed, 0, 2))
+    per = dt / n
+    return max(2, int(seconds / per))
+
+
+# --------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index, period=0.02):
+        self.samples, self.reasons, self.stop_evt = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.period = period
+        self.th = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_evt.set()
+        if self.nv:
+            self.th.join()
+
+    def result(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def fma_per_frame(cfg, tx, ty):
+    """FFMA count per frame of the blur as planned (V pass on the halo-extended
+    columns, H pass on the ring-extended tile), ignoring zero-tile skips."""
+    h, w = cfg.sensor.image_size
+    total = 0
+    for y0 in range(0, h, ty):
+        for x0 in range(0, w, tx):
+            x1, y1 = min(x0 + tx, w), min(y0 + ty, h)
+            ex0, ex1, ey0, ey1 = max(x0 - 1, 0), min(x1 + 1, w), max(y0 - 1, 0), min(y1 + 1, h)
+            EW, EH = ex1 - ex0, ey1 - ey0
+            for _, r in cfg.levels:
+                if r:
+                    total += EH * (EW + 2 * r) * (2 * r + 1) + EH * EW * (2 * r + 1)
+    return total
+
+
+def algorithmic_bytes(cfg):
+    h, w = cfg.sensor.image_size
+    r, c = cfg.sensor.marker_grid
+    return 4 * h * w + 3 * h * w + 8 * r * c + 32
+
+
+# --------------------------------------------------------------------------- arms
+def run_reference(a, rank, world):
+    """--impl reference: the oracle port of the reference CPU path on all host cores."""
+    if rank != 0:
+        return
+    cores = host_cores()
+    fpc = calibrate_frames_per_core(a.config, a.seed, 0.75)
+    for _ in range(a.warmup):
+        cpu_rate(a.config, a.seed, cores, max(1, fpc // 4))
+    vals, walls = [], []
+    for _ in range(a.steps):
+        frames, agg, per_core, wall = cpu_rate(a.config, a.seed, cores, fpc)
+        vals.append(agg)
+        walls.append(wall)
+    v = statistics.median(vals)
+    from paper_2411_04776_b200 import synthetic
+
+    cfg, n_env = synthetic.baseline_config(a.config, a.seed)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": 1e3 * statistics.median(walls),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"configs[{a.config}] sample", "envs_per_step": cores * fpc,
+                   "H": cfg.sensor.image_size[0], "W": cfg.sensor.image_size[1],
+                   "sigmas": [s for s, _ in cfg.levels], "markers": list(cfg.sensor.marker_grid),
+                   "parallelism": f"cpu x{cores} processes"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{cores}x{fpc} frames of configs[{a.config}] per step, oracle port "
+                                   "(scipy.ndimage blur as REF/tactile.py:219, numpy gradient/LUT/markers), f64"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_04776_b200 import TactilePipeline, synthetic
+    from paper_2411_04776_b200.hostio import HostStreamer, host_observation
+    from paper_2411_04776_b200.sharding import gather_summaries
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg, n_env = synthetic.baseline_config(a.config, a.seed)
+    if a.envs:
+        n_env = a.envs
+    h, w = cfg.sensor.image_size
+    pipe = TactilePipeline(cfg, dev)
+
+    # inputs resident in HBM before the timed region (> L2, see config.l2)
+    params = synthetic.indenters(n_env, h, w, a.seed + 10 + 1000 * rank)
+    depth = synthetic.height_maps(params, h, w, device=dev, dtype=torch.float32, chunk=512)
+    shear_np, twist_np = synthetic.loads(n_env, a.seed + 20 + 1000 * rank)
+    shear = torch.as_tensor(shear_np, device=dev)
+    twist = torch.as_tensor(twist_np, device=dev)
+    out = pipe.allocate(n_env)
+    args = pipe.launch_args(depth, shear, twist, out)
+    gathered = torch.empty((world * n_env, 8), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def step():
+        pipe.launch(args)
+        if world > 1:
+            gather_summaries(out.summary, gathered)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    contact_frac = float((depth < cfg.sensor.gelpad_thickness - cfg.contact_threshold).float().mean())
+
+    stream = torch.cuda.current_stream(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / a.steps
+    value = world * n_env * a.steps / (ms / 1e3)
+
+    # kernel-only launch duration (the fused kernel is the only launch per step)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+    for e0, e1 in kev:
+        e0.record(stream)
+        pipe.launch(args)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in kev)
+
+    # e2e: host buffers through the public host API, copies inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        depth_h = depth.cpu().pin_memory()
+        shear_h = shear.cpu().pin_memory()
+        twist_h = twist.cpu().pin_memory()
+        out_h = host_observation(pipe, n_env)
+        streamer = HostStreamer(pipe, chunk=min(512, n_env))
+        e_steps = max(3, min(20, a.steps // 10))
+        for _ in range(2):
+            streamer.run(depth_h, shear_h, twist_h, out_h)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            streamer.run(depth_h, shear_h, twist_h, out_h)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        r, c = cfg.sensor.marker_grid
+        e2e = {
+            "value": world * n_env * e_steps / (ems / 1e3),
+            "unit": UNIT,
+            "h2d_bytes_per_step": n_env * (4 * h * w + 16 + 8),
+            "d2h_bytes_per_step": n_env * (3 * h * w + 8 * r * c + 32),
+            "steps": e_steps,
+            "path": "hostio.HostStreamer -> TactilePipeline.simulate (tac_pipeline C ABI), pinned host buffers",
+        }
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peak()
+    per_launch = algorithmic_bytes(cfg) * n_env
+    achieved = per_launch / (k_ms / 1e3) / 1e9
+    props = torch.cuda.get_device_properties(dev)
+    clocks = clk.result()
+    fma = fma_per_frame(cfg, int(os.environ.get("TAC_TILE_X", 64)), int(os.environ.get("TAC_TILE_Y", 30)))
+    sm_ghz = (clocks["sm_mhz"] or 1965) / 1e3
+    fma_peak = props.multi_processor_count * 128 * sm_ghz * 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"configs[{a.config}]")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded indenter height maps generated on device; no dataset exists)",
+        "config": {
+            "workload": f"configs[{a.config}]",
+            "envs_per_gpu": n_env,
+            "global_envs": world * n_env,
+            "H": h, "W": w,
+            "sigmas": [s for s, _ in cfg.levels],
+            "lut_bins": list(cfg.lut.shape[:2]),
+            "markers": list(cfg.sensor.marker_grid),
+            "dot_radius": cfg.dot_radius,
+            "parallelism": f"env-sharded x{world}" + (" + NCCL all_gather(summary)" if world > 1 else ""),
+            "l2": f"inputs {n_env * h * w * 4 / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)",
+            "contact_pixel_fraction": round(contact_frac, 4),
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)",
+            "kernel": "frame_kernel<1> (tac_pipeline)",
+            "kernel_ms": k_ms,
+            "algorithmic_bytes_per_frame": algorithmic_bytes(cfg),
+            "fp32_fma": {"per_frame_dense": fma,
+                         "achieved_tflops_dense_equiv": 2 * fma * n_env / (k_ms / 1e3) / 1e12,
+                         "peak_tflops": 2 * fma_peak / 1e12},
+        },
+        "gpu_launches": a.steps,
+        "clocks": clocks,
+        "device": props.name,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not a.no_cpu_baseline:
+        cores = host_cores()
+        fpc = calibrate_frames_per_core(a.config, a.seed, a.cpu_seconds)
+        frames, agg, per_core, wall = cpu_rate(a.config, a.seed, cores, fpc)
+        line["cpu_baseline"] = {
+            "value": agg, "unit": UNIT, "cores": cores, "kind": "port",
+            "per_core": per_core,
+            "sample": f"{frames} frames ({cores}x{fpc}) of configs[{a.config}], oracle port, f64, "
+                      f"{wall:.1f} s wall",
+        }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

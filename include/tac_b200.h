@@ -1,0 +1,183 @@
+/*
+ * tac_b200 — C ABI of the B200-native tactile-image path.
+ *
+ * Drop-in boundary for the per-sensor sensing layer of the reference
+ * `tacsim` package (REF = /root/reference/pkg/src/tacsim).  The reference has
+ * no FFI: its operator API is plain module functions on NumPy arrays,
+ * re-exported at REF/__init__.py:59-81 and called per sensor by
+ * Environment._observe (REF/envs.py:1156-1209) and cmd_render
+ * (REF/cli.py:274-301).  Each entry point below replaces one of those
+ * functions, batched over a leading env dimension; INTEGRATION.md shows the
+ * ctypes binding a maintainer adds on the reference side.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (CUDA global memory), dense,
+ *     row-major, with the leading dimension N = n_env.  fp32 unless noted.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call
+ *     only enqueues work; nothing synchronises the host.
+ *   - The caller owns every buffer.  The library never allocates per call.
+ *     Calls that reduce over a frame take a `workspace` of
+ *     tac_workspace_bytes(ctx, n_env) bytes that must be ZERO-FILLED ONCE when
+ *     allocated; the kernels leave it zeroed again on exit, so a workspace can
+ *     be reused by later calls on the same stream.  Use one workspace per
+ *     concurrently running stream.
+ *   - A context is immutable after creation: calls are reentrant across
+ *     host threads and streams.
+ *   - Return value: TAC_OK or an error status; tac_last_error() returns a
+ *     thread-local message for the last failing call on this thread.  The
+ *     error classes mirror REF/errors.py:6-11 (InvalidArgumentError).
+ *   - There is no CPU fallback inside the library.
+ */
+#ifndef TAC_B200_H
+#define TAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TAC_MAX_LEVELS 8
+#define TAC_MAX_RADIUS 24
+
+enum {
+  TAC_OK = 0,
+  TAC_ERR_INVALID = 1,     /* precondition violated  -> InvalidArgumentError */
+  TAC_ERR_CUDA = 2,        /* CUDA runtime error     -> RuntimeError */
+  TAC_ERR_UNSUPPORTED = 3  /* valid but unsupported configuration */
+};
+
+/* Input kinds for entry points that accept either map. */
+enum {
+  TAC_INPUT_DEPTH = 0,       /* HeightMap values: depth from the camera plane (REF/tactile.py:72-87) */
+  TAC_INPUT_INDENTATION = 1  /* IndentationMap values: penetration >= 0 (REF/tactile.py:90-107) */
+};
+
+/* Load sources for the marker stage of tac_pipeline. */
+enum {
+  TAC_LOAD_GIVEN = 0, /* shear[N,2] (m) and twist[N] (rad) supplied per env */
+  TAC_LOAD_TRACK = 1  /* track_load: state[N,8] advanced by pose_delta[N,3] */
+};
+
+/*
+ * Sensor + optical + marker configuration, uploaded once by tac_ctx_create.
+ * Field sources: SensorConfig REF/tactile.py:31-69; smooth_pyramid levels
+ * REF/tactile.py:200-222; PolyTable / binned LUT REF/optical.py:97-135;
+ * MarkerParams REF/marker.py:25-40; DEFAULT_CONTACT_THRESHOLD REF/marker.py:22;
+ * render_markers REF/marker.py:203-234.
+ */
+typedef struct tac_config {
+  int32_t height, width;    /* image_size (H, W); both >= 2 */
+  double pixel_pitch;       /* m per pixel (square pixels) */
+  double gel_thickness;     /* rest surface depth, m */
+
+  int32_t n_levels;                  /* 1..TAC_MAX_LEVELS */
+  double sigma[TAC_MAX_LEVELS];      /* px; ignored when radius == 0 */
+  int32_t radius[TAC_MAX_LEVELS];    /* 0..TAC_MAX_RADIUS; 0 = identity level (k == 1) */
+
+  int32_t mag_bins, dir_bins;        /* LUT bins (125 x 180 in BASELINE configs) */
+  double g_max;                      /* gradient magnitude mapped to the last magnitude bin */
+  const float* lut;        /* HOST [mag_bins][dir_bins][3][6] fp32, 8-bit units; c0 unused */
+  const float* background; /* HOST [H][W][3] fp32, 8-bit units */
+
+  int32_t marker_rows, marker_cols;  /* marker_grid */
+  const double* rest_grid; /* HOST [rows][cols][2] m, or NULL = grid_rest_positions (REF/marker.py:93-100) */
+  double k_n, lambda_n, lambda_s, k_t, lambda_t; /* MarkerParams */
+  double contact_threshold;          /* > 0 */
+  int32_t dot_radius;                /* 0..12 */
+  uint8_t dot_color[3];
+} tac_config;
+
+typedef struct tac_ctx tac_ctx;
+
+/* Build a context: validates `cfg`, uploads the LUT (repacked), background,
+ * quantised background, Gaussian taps and marker grid to the current device. */
+int tac_ctx_create(const tac_config* cfg, tac_ctx** out);
+int tac_ctx_destroy(tac_ctx* ctx);
+const char* tac_last_error(void);
+/* Bytes of zero-initialised workspace needed by reducing calls for n_env envs. */
+size_t tac_workspace_bytes(const tac_ctx* ctx, int64_t n_env);
+/* Tiles per frame used by the frame kernels (for diagnostics). */
+int32_t tac_tiles_per_frame(const tac_ctx* ctx);
+
+/* indentation_from (REF/tactile.py:193-197): ind = clip(rest - depth, 0, rest).
+ * depth, ind: [N,H,W]. */
+int tac_indentation(const tac_ctx* ctx, const float* depth, float* ind,
+                    int64_t n_env, void* stream);
+
+/* Kernel (a): indentation_from + smooth_pyramid (REF/tactile.py:193-222) with
+ * the context's levels.  in: [N,H,W] of `input_kind`; blurred: [N,H,W].
+ * summary (nullable): [N,8] contact summary as tac_contact. */
+int tac_contact_blur(const tac_ctx* ctx, const float* in, int32_t input_kind,
+                     float* blurred, float* summary, void* workspace,
+                     int64_t n_env, void* stream);
+
+/* normals_from (REF/optical.py:138-163) of an elevation map (IndentationMap
+ * values): elev [N,H,W] -> normals [N,H,W,3]. */
+int tac_normals(const tac_ctx* ctx, const float* elev, float* normals,
+                int64_t n_env, void* stream);
+
+/* Kernel (b): gradient -> bins -> LUT -> + background -> uint8 (shade,
+ * REF/optical.py:233-250, with the binned LUT of DESIGN.md §3 and the uint8
+ * rule of REF/cli.py:134-139).  blurred [N,H,W] -> rgb [N,H,W,3] uint8. */
+int tac_shade(const tac_ctx* ctx, const float* blurred, uint8_t* rgb,
+              int64_t n_env, void* stream);
+
+/* contact_center (REF/marker.py:103-121) on the raw (unsmoothed) map.
+ * contact (nullable): fp64 [N,8] LoadState layout (below) with shear/twist 0,
+ *   exactly what the reference returns;
+ * summary (nullable): fp32 [N,8] = {in_contact, area m^2, c_x m, c_y m,
+ *   d_c m, force proxy m^3 (sum of indentation * p^2 over the contact mask),
+ *   number of non-finite inputs, 0}. */
+int tac_contact(const tac_ctx* ctx, const float* in, int32_t input_kind,
+                double* contact, float* summary, void* workspace, int64_t n_env,
+                void* stream);
+
+/* LoadState layout (REF/marker.py:43-70), fp64 [N,8]:
+ *   {c_x, c_y, d_c, s_x, s_y, twist, in_contact (0/1), 0}. */
+
+/* track_load (REF/marker.py:124-140).  state fp64 [N,8] in/out (LoadState);
+ * pose_delta fp64 [N,3] = {dt_x, dt_y, rotvec_z} of the case pose delta;
+ * contact fp64 [N,8] from tac_contact. */
+int tac_track_load(const tac_ctx* ctx, double* state, const double* pose_delta,
+                   const double* contact, int64_t n_env, void* stream);
+
+/* marker_displacements (REF/marker.py:143-165).  loads fp64 [N,8]
+ * (LoadState) -> disp fp32 [N,rows,cols,2] (m). */
+int tac_marker_displacements(const tac_ctx* ctx, const double* loads, float* disp,
+                             int64_t n_env, void* stream);
+
+/* render_markers dot splat (REF/marker.py:203-234, arrows excluded): draws
+ * filled dots of the context radius / colour at rest + disp into rgb. */
+int tac_render_markers(const tac_ctx* ctx, const float* disp, uint8_t* rgb,
+                       int64_t n_env, void* stream);
+
+/* The fused path: one launch per call.  depth -> rgb (with dots), disp,
+ * summary (+ optional blurred) for every env.  Equivalent to, per env:
+ * indentation_from -> smooth_pyramid -> shade -> uint8 ; contact_center ->
+ * (given load | track_load) -> marker_displacements -> render_markers. */
+typedef struct tac_pipeline_args {
+  const float* in;          /* [N,H,W] */
+  int32_t input_kind;       /* TAC_INPUT_* */
+  int32_t load_mode;        /* TAC_LOAD_* */
+  const double* shear;      /* fp64 [N,2] m   (TAC_LOAD_GIVEN) */
+  const double* twist;      /* fp64 [N]   rad (TAC_LOAD_GIVEN) */
+  double* state;            /* fp64 [N,8] LoadState (TAC_LOAD_TRACK, in/out) */
+  const double* pose_delta; /* fp64 [N,3] (TAC_LOAD_TRACK) */
+  uint8_t* rgb;             /* [N,H,W,3] out */
+  float* disp;              /* [N,rows,cols,2] out, nullable */
+  float* summary;           /* [N,8] out, nullable (tac_contact layout) */
+  double* contact;          /* fp64 [N,8] out, nullable (tac_contact layout) */
+  float* blurred;           /* [N,H,W] out, nullable (parity/debug) */
+  int32_t splat;            /* nonzero: draw marker dots into rgb */
+  void* workspace;
+  int64_t n_env;
+} tac_pipeline_args;
+
+int tac_pipeline(const tac_ctx* ctx, const tac_pipeline_args* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAC_B200_H */

@@ -1,0 +1,155 @@
+"""Configuration types mirroring the reference dataclasses.
+
+``SensorConfig`` mirrors REF/tactile.py:31-69, ``MarkerParams`` mirrors
+REF/marker.py:25-40 (same defaults, same validation, same error class).
+``PipelineConfig`` is the frozen bundle uploaded once into a C-ABI context.
+"""
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from .errors import InvalidArgumentError
+
+DEFAULT_PYRAMID = (5, 11, 21, 31)  # REF/tactile.py:22
+DEFAULT_CONTACT_THRESHOLD = 5e-5  # REF/marker.py:22
+
+
+@dataclass(frozen=True)
+class SensorConfig:
+    """Geometry of one tactile sensor (REF/tactile.py:31-69)."""
+
+    image_size: Tuple[int, int] = (480, 640)
+    sensing_area: Tuple[float, float] = (0.016, 0.012)
+    gelpad_thickness: float = 0.004
+    marker_grid: Tuple[int, int] = (10, 10)
+
+    def __post_init__(self):
+        h, w = self.image_size
+        if int(h) <= 0 or int(w) <= 0:
+            raise InvalidArgumentError("image_size must be positive")
+        aw, ah = self.sensing_area
+        if aw <= 0 or ah <= 0:
+            raise InvalidArgumentError("sensing_area must be positive")
+        if self.gelpad_thickness <= 0:
+            raise InvalidArgumentError("gelpad_thickness must be positive")
+        if int(self.marker_grid[0]) <= 0 or int(self.marker_grid[1]) <= 0:
+            raise InvalidArgumentError("marker_grid must be positive")
+        if abs(aw / w - ah / h) > 1e-12:
+            raise InvalidArgumentError("sensing_area and image_size imply unequal x/y pixel pitch")
+
+    @property
+    def pixel_pitch(self) -> float:
+        return self.sensing_area[0] / self.image_size[1]
+
+    @staticmethod
+    def from_pitch(h, w, pitch, gelpad_thickness=0.004, marker_grid=(10, 10)):
+        return SensorConfig((int(h), int(w)), (w * pitch, h * pitch), gelpad_thickness, marker_grid)
+
+
+@dataclass(frozen=True)
+class MarkerParams:
+    """Displacement-distribution constants, metres (REF/marker.py:25-40)."""
+
+    k_n: float = 0.3
+    lambda_n: float = 4e-3
+    lambda_s: float = 5e-3
+    k_t: float = 0.5
+    lambda_t: float = 4e-3
+
+    def __post_init__(self):
+        vals = (self.k_n, self.lambda_n, self.lambda_s, self.k_t, self.lambda_t)
+        if not all(math.isfinite(v) for v in vals):
+            raise InvalidArgumentError("marker params must be finite")
+        if self.lambda_n <= 0 or self.lambda_s <= 0 or self.lambda_t <= 0:
+            raise InvalidArgumentError("marker length scales must be positive")
+
+
+def levels_from_kernel_sizes(kernel_sizes: Sequence[int] = DEFAULT_PYRAMID):
+    """(sigma, radius) per level, REF/tactile.py:204-218 (same validation)."""
+    sizes = [int(k) for k in kernel_sizes]
+    if not sizes:
+        raise InvalidArgumentError("kernel_sizes must be nonempty")
+    for k in sizes:
+        if k < 1 or k % 2 == 0:
+            raise InvalidArgumentError("kernel sizes must be odd and >= 1")
+    if sizes != sorted(sizes):
+        raise InvalidArgumentError("kernel sizes must be ascending")
+    return tuple((0.0, 0) if k == 1 else (k / 6.0, (k - 1) // 2) for k in sizes)
+
+
+def levels_from_sigmas(sigmas: Sequence[float], truncate: float = 3.0):
+    """(sigma, radius = ceil(truncate * sigma)) per level: the north star's
+    sigma-keyed pyramid.  sigma 0 = identity level."""
+    out = []
+    if not len(sigmas):
+        raise InvalidArgumentError("sigmas must be nonempty")
+    for s in sigmas:
+        s = float(s)
+        if not math.isfinite(s) or s < 0:
+            raise InvalidArgumentError("sigma must be finite and >= 0")
+        out.append((0.0, 0) if s == 0 else (s, int(math.ceil(truncate * s - 1e-12))))
+    return tuple(out)
+
+
+def grid_rest_positions(cfg: SensorConfig) -> np.ndarray:
+    """(rows, cols, 2) marker rest grid, REF/marker.py:93-100."""
+    rows, cols = int(cfg.marker_grid[0]), int(cfg.marker_grid[1])
+    w, h = cfg.sensing_area
+    xs = ((np.arange(cols) + 0.5) / cols - 0.5) * w
+    ys = ((np.arange(rows) + 0.5) / rows - 0.5) * h
+    gx, gy = np.meshgrid(xs, ys)
+    return np.stack([gx, gy], axis=-1)
+
+
+@dataclass(frozen=True, eq=False)
+class PipelineConfig:
+    """Everything the sm_100a path needs, uploaded once per context.
+
+    lut: (mag_bins, dir_bins, 3, 6) float32, 8-bit units, basis order of
+    REF/optical.py:82-88 (c0 ignored: it cancels, REF/optical.py:244).
+    background: (H, W, 3) float32 in 8-bit units.
+    """
+
+    sensor: SensorConfig
+    levels: Tuple[Tuple[float, int], ...]
+    lut: np.ndarray
+    background: np.ndarray
+    g_max: float = 1.0
+    marker_params: MarkerParams = field(default_factory=MarkerParams)
+    contact_threshold: float = DEFAULT_CONTACT_THRESHOLD
+    dot_radius: int = 3
+    dot_color: Tuple[int, int, int] = (25, 25, 25)
+    rest_grid: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        h, w = self.sensor.image_size
+        lut = np.ascontiguousarray(self.lut, dtype=np.float32)
+        bg = np.ascontiguousarray(self.background, dtype=np.float32)
+        if lut.ndim != 4 or lut.shape[2:] != (3, 6):
+            raise InvalidArgumentError("lut must be (mag_bins, dir_bins, 3, 6)")
+        if bg.shape != (h, w, 3):
+            raise InvalidArgumentError("background must be (H, W, 3)")
+        if not (np.isfinite(lut).all() and np.isfinite(bg).all()):
+            raise InvalidArgumentError("table values must be finite")
+        if not (self.g_max > 0 and math.isfinite(self.g_max)):
+            raise InvalidArgumentError("g_max must be positive")
+        if self.contact_threshold <= 0:
+            raise InvalidArgumentError("threshold must be positive")
+        if not self.levels:
+            raise InvalidArgumentError("pyramid needs at least one level")
+        object.__setattr__(self, "lut", lut)
+        object.__setattr__(self, "background", bg)
+        grid = self.rest_grid
+        if grid is None:
+            grid = grid_rest_positions(self.sensor)
+        grid = np.ascontiguousarray(grid, dtype=np.float64)
+        if grid.shape != (self.sensor.marker_grid[0], self.sensor.marker_grid[1], 2):
+            raise InvalidArgumentError("rest_positions must be (rows, cols, 2)")
+        object.__setattr__(self, "rest_grid", grid)
+
+    @property
+    def pixel_pitch(self):
+        return self.sensor.pixel_pitch

@@ -1,0 +1,434 @@
+// C ABI: context lifetime, argument validation (error classes of
+// REF/errors.py), and kernel launches.  No CPU fallback: every compute entry
+// point enqueues CUDA work on the caller's stream or returns an error.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tac_internal.cuh"
+
+using namespace tac;
+
+struct tac_ctx {
+  tac_config cfg;  // host pointers cleared after upload
+  int device;
+  float4* d_lut = nullptr;
+  float* d_bg = nullptr;
+  uint8_t* d_bg_u8 = nullptr;
+  double* d_grid = nullptr;
+  FrameParams fused, blur, contact;  // per-mode launch templates
+  MarkerGeom mg;
+  int max_tiles;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(TAC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
+
+int env_int(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  if (!s || !*s) return dflt;
+  return std::atoi(s);
+}
+
+// Fill geometry/pitches of a frame-kernel template for a tile size.
+void plan_tiles(FrameParams& p, int mode, int TX, int TY) {
+  p.TX = std::min(TX, p.W);
+  p.TY = std::min(TY, p.H);
+  p.tiles_x = (p.W + p.TX - 1) / p.TX;
+  p.tiles_y = (p.H + p.TY - 1) / p.TY;
+  const int ring = (mode == kModeFused) ? 1 : 0;
+  const int R = (mode == kModeContact) ? 0 : p.R;
+  p.ring = ring;
+  const int EWm = p.TX + 2 * ring, EHm = p.TY + 2 * ring;
+  const int WWm = EWm + 2 * R;
+  int wp = WWm + K;
+  if ((wp & 1) == 0) ++wp;  // odd pitch: row-strided lanes hit distinct banks
+  p.win_pitch = wp;
+  p.win_rows = EHm + 2 * R + K;
+  int ap = EWm + K;
+  if ((ap & 1) == 0) ++ap;
+  p.acc_pitch = ap;
+  p.acc_rows = EHm;
+  if (mode == kModeContact) {
+    // window only; no vbuf / acc needed
+    p.acc_rows = 0;
+  }
+}
+
+int free_ctx(tac_ctx* c) {
+  if (!c) return TAC_OK;
+  cudaFree(c->d_lut);
+  cudaFree(c->d_bg);
+  cudaFree(c->d_bg_u8);
+  cudaFree(c->d_grid);
+  delete c;
+  return TAC_OK;
+}
+
+int check_device(const tac_ctx* c) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev != c->device)
+    return fail(TAC_ERR_INVALID, "context was created on device %d but the current device is %d",
+                c->device, dev);
+  return TAC_OK;
+}
+
+int common_checks(const tac_ctx* c, int64_t n_env) {
+  if (!c) return fail(TAC_ERR_INVALID, "null context");
+  if (n_env < 0) return fail(TAC_ERR_INVALID, "n_env must be >= 0");
+  if (n_env > (int64_t)0x7fffffff / std::max(1, c->max_tiles))
+    return fail(TAC_ERR_UNSUPPORTED, "n_env too large for one launch");
+  return check_device(c);
+}
+
+void bind_workspace(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) {
+  p.partials = reinterpret_cast<float*>(ws);
+  const size_t part_bytes = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(float)) + 255) & ~size_t(255);
+  p.counters = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + part_bytes);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tac_last_error(void) { return g_err.c_str(); }
+
+int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
+  if (!cfg || !out) return fail(TAC_ERR_INVALID, "null argument");
+  *out = nullptr;
+  const tac_config& k = *cfg;
+  if (k.height < 2 || k.width < 2) return fail(TAC_ERR_INVALID, "image_size must be >= 2 x 2");
+  if (!finite_pos(k.pixel_pitch)) return fail(TAC_ERR_INVALID, "pixel_pitch must be positive");
+  if (!finite_pos(k.gel_thickness)) return fail(TAC_ERR_INVALID, "gelpad_thickness must be positive");
+  if (k.n_levels < 1 || k.n_levels > TAC_MAX_LEVELS)
+    return fail(TAC_ERR_INVALID, "pyramid needs 1..%d levels", TAC_MAX_LEVELS);
+  int R = 0;
+  for (int l = 0; l < k.n_levels; ++l) {
+    if (k.radius[l] < 0) return fail(TAC_ERR_INVALID, "radius must be >= 0");
+    if (k.radius[l] > TAC_MAX_RADIUS)
+      return fail(TAC_ERR_UNSUPPORTED, "radius %d exceeds TAC_MAX_RADIUS=%d", k.radius[l], TAC_MAX_RADIUS);
+    if (k.radius[l] > 0 && !finite_pos(k.sigma[l])) return fail(TAC_ERR_INVALID, "sigma must be positive");
+    R = std::max(R, k.radius[l]);
+  }
+  if (k.mag_bins < 1 || k.dir_bins < 1) return fail(TAC_ERR_INVALID, "LUT bins must be >= 1");
+  if (!finite_pos(k.g_max)) return fail(TAC_ERR_INVALID, "g_max must be positive");
+  if (!k.lut || !k.background) return fail(TAC_ERR_INVALID, "lut and background are required");
+  if (k.marker_rows < 1 || k.marker_cols < 1) return fail(TAC_ERR_INVALID, "marker_grid must be positive");
+  const double lam[3] = {k.lambda_n, k.lambda_s, k.lambda_t};
+  for (double v : lam)
+    if (!finite_pos(v)) return fail(TAC_ERR_INVALID, "marker length scales must be positive");
+  if (!std::isfinite(k.k_n) || !std::isfinite(k.k_t)) return fail(TAC_ERR_INVALID, "marker params must be finite");
+  if (!finite_pos(k.contact_threshold)) return fail(TAC_ERR_INVALID, "threshold must be positive");
+  if (k.dot_radius < 0 || k.dot_radius > 32) return fail(TAC_ERR_UNSUPPORTED, "dot_radius must be in 0..32");
+  const size_t HW = (size_t)k.height * k.width;
+  for (size_t i = 0; i < HW * 3; ++i)
+    if (!std::isfinite(k.background[i])) return fail(TAC_ERR_INVALID, "table values must be finite");
+  const size_t nbins = (size_t)k.mag_bins * k.dir_bins;
+  for (size_t i = 0; i < nbins * 18; ++i)
+    if (!std::isfinite(k.lut[i])) return fail(TAC_ERR_INVALID, "table values must be finite");
+
+  tac_ctx* c = new tac_ctx();
+  c->cfg = k;
+  c->cfg.lut = nullptr;
+  c->cfg.background = nullptr;
+  c->cfg.rest_grid = nullptr;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    return cuda_fail(e, "cudaGetDevice");
+  }
+
+  // LUT: [mag][dir][3][6] -> [mag*dir][16] = c1..c5 per channel + pad
+  std::vector<float> lut(nbins * 16, 0.f);
+  for (size_t b = 0; b < nbins; ++b)
+    for (int ch = 0; ch < 3; ++ch)
+      for (int t = 1; t < 6; ++t) lut[b * 16 + ch * 5 + (t - 1)] = k.lut[(b * 3 + ch) * 6 + t];
+  std::vector<uint8_t> bgq(HW * 3);
+  for (size_t i = 0; i < HW * 3; ++i) {
+    long v = std::lrint((double)k.background[i]);  // half-to-even (default rounding mode)
+    bgq[i] = (uint8_t)std::min(255L, std::max(0L, v));
+  }
+  const int nm = k.marker_rows * k.marker_cols;
+  std::vector<double> grid(nm * 2);
+  if (cfg->rest_grid) {
+    std::memcpy(grid.data(), cfg->rest_grid, sizeof(double) * nm * 2);
+  } else {
+    // grid_rest_positions, REF/marker.py:93-100; sensing area = (W p, H p)
+    const double aw = k.width * k.pixel_pitch, ah = k.height * k.pixel_pitch;
+    for (int i = 0; i < k.marker_rows; ++i)
+      for (int j = 0; j < k.marker_cols; ++j) {
+        grid[(i * k.marker_cols + j) * 2 + 0] = ((j + 0.5) / k.marker_cols - 0.5) * aw;
+        grid[(i * k.marker_cols + j) * 2 + 1] = ((i + 0.5) / k.marker_rows - 0.5) * ah;
+      }
+  }
+  struct Up {
+    void** dst;
+    const void* src;
+    size_t bytes;
+  } ups[] = {
+      {(void**)&c->d_lut, lut.data(), lut.size() * sizeof(float)},
+      {(void**)&c->d_bg, k.background, HW * 3 * sizeof(float)},
+      {(void**)&c->d_bg_u8, bgq.data(), bgq.size()},
+      {(void**)&c->d_grid, grid.data(), grid.size() * sizeof(double)},
+  };
+  for (auto& u : ups) {
+    e = cudaMalloc(u.dst, u.bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(*u.dst, u.src, u.bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return cuda_fail(e, "context upload");
+    }
+  }
+
+  MarkerGeom& mg = c->mg;
+  mg.H = k.height;
+  mg.W = k.width;
+  mg.pitch = k.pixel_pitch;
+  mg.rows = k.marker_rows;
+  mg.cols = k.marker_cols;
+  mg.rest_grid = c->d_grid;
+  mg.k_n = k.k_n;
+  mg.lambda_n = k.lambda_n;
+  mg.lambda_s = k.lambda_s;
+  mg.k_t = k.k_t;
+  mg.lambda_t = k.lambda_t;
+  mg.dot_radius = k.dot_radius;
+  mg.dot_r = k.dot_color[0];
+  mg.dot_g = k.dot_color[1];
+  mg.dot_b = k.dot_color[2];
+
+  FrameParams b;
+  std::memset(&b, 0, sizeof(b));
+  b.H = k.height;
+  b.W = k.width;
+  b.R = R;
+  b.n_levels = k.n_levels;
+  for (int l = 0; l < k.n_levels; ++l) {
+    const int r = k.radius[l];
+    b.radius[l] = r;
+    // gaussian taps exactly as scipy's _gaussian_kernel1d, in fp64
+    std::vector<double> w(r + 1);
+    if (r == 0) {
+      w[0] = 1.0;
+    } else {
+      double sum = 0.0;
+      const double s2 = k.sigma[l] * k.sigma[l];
+      std::vector<double> phi(2 * r + 1);
+      for (int x = -r; x <= r; ++x) {
+        phi[x + r] = std::exp(-0.5 / s2 * (double)x * (double)x);
+        sum += phi[x + r];
+      }
+      for (int i = 0; i <= r; ++i) w[i] = phi[r + i] / sum;
+    }
+    for (int i = 0; i <= r; ++i) {
+      b.wv[l][i] = (float)w[i];
+      b.wh[l][i] = (float)(w[i] / k.n_levels);
+    }
+  }
+  b.rest = (float)k.gel_thickness;
+  b.rest_lo = (float)(k.gel_thickness - (double)b.rest);
+  b.threshold = (float)k.contact_threshold;
+  b.half_w = 0.5f * k.width;
+  b.half_h = 0.5f * k.height;
+  b.inv_p = (float)(1.0 / k.pixel_pitch);
+  b.inv_2p = (float)(1.0 / (2.0 * k.pixel_pitch));
+  b.mag_scale = (float)(k.mag_bins / k.g_max);
+  b.dir_scale = (float)(k.dir_bins / (2.0 * M_PI));
+  b.mag_bins = k.mag_bins;
+  b.dir_bins = k.dir_bins;
+  b.lut = c->d_lut;
+  b.bg = c->d_bg;
+  b.bg_u8 = c->d_bg_u8;
+  b.mg = mg;
+
+  const int tx = env_int("TAC_TILE_X", 64), ty = env_int("TAC_TILE_Y", 30);
+  c->fused = b;
+  plan_tiles(c->fused, kModeFused, tx, ty);
+  c->blur = b;
+  plan_tiles(c->blur, kModeBlur, tx, ty + 2);
+  c->contact = b;
+  plan_tiles(c->contact, kModeContact, std::max(tx, 64), 32);
+  c->max_tiles = std::max({c->fused.tiles_x * c->fused.tiles_y, c->blur.tiles_x * c->blur.tiles_y,
+                           c->contact.tiles_x * c->contact.tiles_y});
+  for (int mode = 0; mode < 3; ++mode) {
+    FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
+    if (frame_smem_bytes(p, mode) > 227 * 1024) {
+      free_ctx(c);
+      return fail(TAC_ERR_UNSUPPORTED, "tile %dx%d with radius %d needs %zu B of shared memory",
+                  p.TX, p.TY, R, frame_smem_bytes(p, mode));
+    }
+  }
+  *out = c;
+  return TAC_OK;
+}
+
+int tac_ctx_destroy(tac_ctx* ctx) { return free_ctx(ctx); }
+
+size_t tac_workspace_bytes(const tac_ctx* c, int64_t n_env) {
+  if (!c || n_env < 0) return 0;
+  const size_t part = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(float)) + 255) & ~size_t(255);
+  return part + (((size_t)n_env * sizeof(unsigned int) + 255) & ~size_t(255));
+}
+
+int32_t tac_tiles_per_frame(const tac_ctx* c) {
+  return c ? c->fused.tiles_x * c->fused.tiles_y : 0;
+}
+
+int tac_indentation(const tac_ctx* c, const float* depth, float* ind, int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_env && (!depth || !ind)) return fail(TAC_ERR_INVALID, "null buffer");
+  cudaError_t e = launch_indentation(depth, ind, c->fused.rest, c->fused.rest_lo,
+                                     n_env * (long long)c->cfg.height * c->cfg.width,
+                                     (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_indentation");
+}
+
+int tac_contact_blur(const tac_ctx* c, const float* in, int32_t input_kind, float* blurred,
+                     float* summary, void* workspace, int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (input_kind != TAC_INPUT_DEPTH && input_kind != TAC_INPUT_INDENTATION)
+    return fail(TAC_ERR_INVALID, "unknown input_kind %d", input_kind);
+  if (n_env && (!in || !blurred)) return fail(TAC_ERR_INVALID, "null buffer");
+  if (summary && !workspace) return fail(TAC_ERR_INVALID, "summary needs a workspace");
+  FrameParams p = c->blur;
+  p.in = in;
+  p.input_depth = input_kind == TAC_INPUT_DEPTH;
+  p.blurred = blurred;
+  p.n_env = n_env;
+  p.finalize = summary ? 1 : 0;
+  p.summary = summary;
+  if (summary) bind_workspace(c, p, workspace, n_env);
+  cudaError_t e = launch_frame(p, kModeBlur, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_contact_blur");
+}
+
+int tac_normals(const tac_ctx* c, const float* elev, float* normals, int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_env && (!elev || !normals)) return fail(TAC_ERR_INVALID, "null buffer");
+  cudaError_t e = launch_normals(elev, normals, c->cfg.height, c->cfg.width, c->fused.inv_p,
+                                 c->fused.inv_2p, n_env, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_normals");
+}
+
+int tac_shade(const tac_ctx* c, const float* blurred, uint8_t* rgb, int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_env && (!blurred || !rgb)) return fail(TAC_ERR_INVALID, "null buffer");
+  FrameParams p = c->fused;
+  p.n_env = n_env;
+  cudaError_t e = launch_shade(p, blurred, rgb, n_env, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_shade");
+}
+
+int tac_contact(const tac_ctx* c, const float* in, int32_t input_kind, double* contact,
+                float* summary, void* workspace, int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (input_kind != TAC_INPUT_DEPTH && input_kind != TAC_INPUT_INDENTATION)
+    return fail(TAC_ERR_INVALID, "unknown input_kind %d", input_kind);
+  if (n_env && !in) return fail(TAC_ERR_INVALID, "null buffer");
+  if (!workspace) return fail(TAC_ERR_INVALID, "tac_contact needs a workspace");
+  FrameParams p = c->contact;
+  p.in = in;
+  p.input_depth = input_kind == TAC_INPUT_DEPTH;
+  p.n_env = n_env;
+  p.finalize = 1;
+  p.summary = summary;
+  p.contact = contact;
+  bind_workspace(c, p, workspace, n_env);
+  cudaError_t e = launch_frame(p, kModeContact, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_contact");
+}
+
+int tac_track_load(const tac_ctx* c, double* state, const double* pose_delta, const double* contact,
+                   int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_env && (!state || !pose_delta || !contact)) return fail(TAC_ERR_INVALID, "null buffer");
+  cudaError_t e = launch_track_load(state, pose_delta, contact, n_env, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_track_load");
+}
+
+int tac_marker_displacements(const tac_ctx* c, const double* loads, float* disp, int64_t n_env,
+                             void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_env && (!loads || !disp)) return fail(TAC_ERR_INVALID, "null buffer");
+  cudaError_t e = launch_marker_displacements(c->mg, loads, disp, n_env, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_marker_displacements");
+}
+
+int tac_render_markers(const tac_ctx* c, const float* disp, uint8_t* rgb, int64_t n_env,
+                       void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_env && (!disp || !rgb)) return fail(TAC_ERR_INVALID, "null buffer");
+  cudaError_t e = launch_render_markers(c->mg, disp, rgb, n_env, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_render_markers");
+}
+
+int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
+  if (!a) return fail(TAC_ERR_INVALID, "null args");
+  int st = common_checks(c, a->n_env);
+  if (st) return st;
+  if (a->input_kind != TAC_INPUT_DEPTH && a->input_kind != TAC_INPUT_INDENTATION)
+    return fail(TAC_ERR_INVALID, "unknown input_kind %d", a->input_kind);
+  if (a->n_env && (!a->in || !a->rgb)) return fail(TAC_ERR_INVALID, "in and rgb are required");
+  if (!a->workspace) return fail(TAC_ERR_INVALID, "tac_pipeline needs a workspace");
+  if (a->load_mode == TAC_LOAD_GIVEN) {
+    if (a->n_env && (!a->shear || !a->twist)) return fail(TAC_ERR_INVALID, "shear and twist are required");
+  } else if (a->load_mode == TAC_LOAD_TRACK) {
+    if (a->n_env && (!a->state || !a->pose_delta))
+      return fail(TAC_ERR_INVALID, "state and pose_delta are required");
+  } else {
+    return fail(TAC_ERR_INVALID, "unknown load_mode %d", a->load_mode);
+  }
+  FrameParams p = c->fused;
+  p.in = a->in;
+  p.input_depth = a->input_kind == TAC_INPUT_DEPTH;
+  p.rgb = a->rgb;
+  p.blurred = a->blurred;
+  p.n_env = a->n_env;
+  p.finalize = 2;
+  p.summary = a->summary;
+  p.contact = a->contact;
+  p.load_mode = a->load_mode;
+  p.shear = a->shear;
+  p.twist = a->twist;
+  p.state = a->state;
+  p.pose_delta = a->pose_delta;
+  p.disp = a->disp;
+  p.splat = a->splat;
+  bind_workspace(c, p, a->workspace, a->n_env);
+  cudaError_t e = launch_frame(p, kModeFused, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_pipeline");
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Internal device-side structures shared by the kernels and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tac_b200.h"
+
+namespace tac {
+
+// Register-blocking factor of the separable passes: each thread produces K
+// consecutive outputs along the pass direction, so every shared-memory load
+// feeds up to K FFMAs.
+constexpr int K = 8;
+constexpr int kThreads = 256;
+constexpr int kSumFields = 8;  // per-tile partial / per-env summary width
+
+// Frame-kernel modes.
+enum FrameMode : int {
+  kModeBlur = 0,     // kernel (a) alone: writes blurred
+  kModeFused = 1,    // kernel (a)+(b): blurred stays in smem, writes uint8 RGB
+  kModeContact = 2,  // reduction only (contact_center)
+};
+
+// Marker geometry + model constants (REF/marker.py:25-40, :93-100, :203-234).
+struct MarkerGeom {
+  int H, W;
+  double pitch;
+  int rows, cols;
+  const double* rest_grid;  // device [rows*cols][2] m
+  double k_n, lambda_n, lambda_s, k_t, lambda_t;
+  int dot_radius;
+  unsigned char dot_r, dot_g, dot_b;
+};
+
+// Everything a frame kernel needs, passed by value (constant bank).
+struct FrameParams {
+  // geometry
+  int H, W;
+  int TX, TY;            // output tile
+  int tiles_x, tiles_y;  // tiles per frame = tiles_x * tiles_y
+  int R;                 // max radius over levels (window halo)
+  int ring;              // 1 when shading is fused (gradient needs +-1), else 0
+  int win_pitch, acc_pitch;  // smem pitches (floats); vbuf uses win_pitch
+  int win_rows;          // allocated window rows (incl. K pad rows)
+  int acc_rows;
+  // pyramid
+  int n_levels;
+  int radius[TAC_MAX_LEVELS];
+  float wv[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // first (vertical) pass taps, centre first
+  float wh[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // second (horizontal) pass taps, folded with 1/L
+  // clamp / contact
+  float rest;           // gel thickness rounded to fp32
+  float rest_lo;        // rest - (double)rest: the clamp runs in ~fp64 accuracy
+  float threshold;
+  float half_w, half_h;  // W/2, H/2 (pixel-centre coordinates)
+  // shading
+  float inv_p, inv_2p;
+  float mag_scale;       // mag_bins / g_max
+  float dir_scale;       // dir_bins / (2 pi)
+  int mag_bins, dir_bins;
+  const float4* lut;     // [mag*dir][4] float4 = c1..c5 per channel (15 used)
+  const float* bg;       // [H][W][3] 8-bit units
+  const uint8_t* bg_u8;  // [H][W][3] = clamp(rint(bg))
+  // io
+  const float* in;
+  int input_depth;
+  float* blurred;        // nullable
+  uint8_t* rgb;          // fused mode
+  float* partials;       // workspace [N][T][8]
+  unsigned int* counters;// workspace [N]
+  long long n_env;
+  // finalize (last CTA of an env)
+  int finalize;          // 0 none, 1 contact/summary, 2 + markers
+  float* summary;        // nullable [N][8]
+  double* contact;       // nullable [N][8] fp64 LoadState
+  // markers
+  MarkerGeom mg;
+  int load_mode;
+  const double* shear;
+  const double* twist;
+  double* state;
+  const double* pose_delta;
+  float* disp;           // nullable
+  int splat;
+};
+
+size_t frame_smem_bytes(const FrameParams& p, int mode);
+cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
+cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,
+                               cudaStream_t s);
+cudaError_t launch_normals(const float* elev, float* normals, int H, int W, float inv_p,
+                           float inv_2p, long long n_env, cudaStream_t s);
+cudaError_t launch_shade(const FrameParams& p, const float* blurred, uint8_t* rgb,
+                         long long n_env, cudaStream_t s);
+cudaError_t launch_track_load(double* state, const double* pose_delta, const double* contact,
+                              long long n_env, cudaStream_t s);
+cudaError_t launch_marker_displacements(const MarkerGeom& m, const double* loads,
+                                        float* disp, long long n_env, cudaStream_t s);
+cudaError_t launch_render_markers(const MarkerGeom& m, const float* disp, uint8_t* rgb,
+                                  long long n_env, cudaStream_t s);
+cudaError_t launch_quantize_bg(const float* bg, uint8_t* bg_u8, long long n, cudaStream_t s);
+
+}  // namespace tac

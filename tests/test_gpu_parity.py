@@ -1,0 +1,390 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Bars (BASELINE.json north_star): uint8 RGB within 1 LSB on >= 99.9% of
+pixels; blurred heights and marker displacements within 1e-4 relative
+(normwise: ||got - ref||_inf <= 1e-4 ||ref||_inf); integer/byte outputs of
+the reference-pinned cases bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import marker as omk
+from oracle import optical as oop
+from oracle import tactile as otac
+from paper_2411_04776_b200 import (
+    IndentationMap,
+    HeightMap,
+    InvalidArgumentError,
+    PipelineConfig,
+    SensorConfig,
+    TactilePipeline,
+    contact_center,
+    indentation_from,
+    levels_from_kernel_sizes,
+    marker_config,
+    marker_displacements,
+    normals_from,
+    render_markers,
+    shade,
+    smooth_pyramid,
+    track_load,
+)
+from paper_2411_04776_b200 import synthetic
+from paper_2411_04776_b200.config import MarkerParams
+
+from _helpers import depth_batch, normwise, oracle_env, rgb_stats, small_config
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+BLUR_TOL = 1e-4
+DISP_TOL = 1e-4
+RGB_FRAC = 0.999
+
+
+def run_pipeline(cfg, depth, shear, twist, **kw):
+    pipe = TactilePipeline(cfg, DEV)
+    d = depth.to(DEV)
+    obs = pipe.simulate(
+        d,
+        torch.as_tensor(shear, dtype=torch.float64, device=DEV),
+        torch.as_tensor(twist, dtype=torch.float64, device=DEV),
+        blurred=True,
+        contact=True,
+        **kw,
+    )
+    torch.cuda.synchronize()
+    return obs
+
+
+def check_env(cfg, depth_np, obs, i, shear, twist, splat=True):
+    ref = oracle_env(cfg, depth_np, shear, twist, splat=splat)
+    b = obs.blurred[i].cpu().numpy()
+    assert normwise(b, ref["blurred"]) <= BLUR_TOL, normwise(b, ref["blurred"])
+    mx, frac = rgb_stats(obs.rgb[i].cpu().numpy(), ref["rgb"])
+    assert frac >= RGB_FRAC, (mx, frac)
+    assert normwise(obs.disp[i].cpu().numpy(), ref["disp"]) <= DISP_TOL
+    s = obs.summary[i].cpu().numpy()
+    rs = ref["summary"]
+    assert s[0] == rs[0]
+    assert abs(s[1] - rs[1]) <= 1e-6 * max(rs[1], 1e-30)  # exact count * p^2 in fp32
+    for k in (2, 3):
+        assert abs(s[k] - rs[k]) <= 1e-6 * cfg.pixel_pitch * max(cfg.sensor.image_size)
+    assert abs(s[4] - rs[4]) <= 1e-6 * max(rs[4], 1e-12)
+    assert abs(s[5] - rs[5]) <= 1e-5 * max(rs[5], 1e-30)
+    return ref
+
+
+class TestPipelineParity:
+    @pytest.mark.parametrize("kind", list(synthetic.KINDS))
+    def test_small_frames_each_primitive(self, kind):
+        cfg = small_config(48, 64)
+        n = 6
+        depth = depth_batch(n, 48, 64, seed=3, fixed_kind=kind, pitch=synthetic.PITCH)
+        shear, twist = synthetic.loads(n, 5)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        for i in range(n):
+            check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
+
+    def test_config0_shape(self):
+        """configs[0]: 240x320 sphere r=4 mm, 0.5 mm, sigma (1,2,4), 7x9 markers, zero shear."""
+        cfg, _ = synthetic.baseline_config(0)
+        depth = depth_batch(2, 240, 320, seed=11, fixed_kind="sphere", pen=0.5e-3)
+        obs = run_pipeline(cfg, depth, np.zeros((2, 2)), np.zeros(2))
+        for i in range(2):
+            check_env(cfg, depth[i].numpy(), obs, i, (0.0, 0.0), 0.0)
+
+    def test_config2_mixed_batch(self):
+        """configs[1]/[2] workload: 4 primitives, pen U(0, 1.2 mm), shear/twist."""
+        cfg, _ = synthetic.baseline_config(2)
+        n = 12
+        depth = depth_batch(n, 240, 320, seed=21)
+        shear, twist = synthetic.loads(n, 22)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        worst = 1.0
+        for i in range(n):
+            ref = oracle_env(cfg, depth[i].numpy(), shear[i], twist[i])
+            _, frac = rgb_stats(obs.rgb[i].cpu().numpy(), ref["rgb"])
+            worst = min(worst, frac)
+            assert normwise(obs.blurred[i].cpu().numpy(), ref["blurred"]) <= BLUR_TOL
+            assert normwise(obs.disp[i].cpu().numpy(), ref["disp"]) <= DISP_TOL
+        assert worst >= RGB_FRAC
+
+    def test_config3_hires_sigma8(self):
+        cfg, _ = synthetic.baseline_config(3)
+        depth = depth_batch(2, 480, 640, seed=31)
+        shear, twist = synthetic.loads(2, 32)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        for i in range(2):
+            check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
+
+    def test_flat_frames_reproduce_background_exactly(self):
+        """Empty scene -> rint(background) bit-exact (REF test_optical.py:286-299,
+        acceptance c5), no contact, zero displacements."""
+        cfg = small_config(40, 56)
+        depth = torch.full((3, 40, 56), synthetic.REST, dtype=torch.float32)
+        obs = run_pipeline(cfg, depth, np.zeros((3, 2)), np.zeros(3), splat=False)
+        bg = np.clip(np.rint(cfg.background.astype(np.float64)), 0, 255).astype(np.uint8)
+        for i in range(3):
+            assert np.array_equal(obs.rgb[i].cpu().numpy(), bg)
+        assert not obs.disp.any()
+        assert not obs.summary[:, 0].any()
+        assert not obs.blurred.any()
+
+    def test_full_contact_plate(self):
+        cfg = small_config(48, 64)
+        depth = torch.full((2, 48, 64), synthetic.REST - 3e-4, dtype=torch.float32)
+        obs = run_pipeline(cfg, depth, np.zeros((2, 2)), np.zeros(2))
+        for i in range(2):
+            ref = check_env(cfg, depth[i].numpy(), obs, i, (0.0, 0.0), 0.0)
+            assert ref["summary"][0] == 1.0
+
+    def test_clamps_beyond_rest_and_camera(self):
+        cfg = small_config(48, 64)
+        rng = np.random.default_rng(4)
+        depth = torch.as_tensor(rng.uniform(-5e-4, synthetic.REST + 5e-4, (2, 48, 64)), dtype=torch.float32)
+        obs = run_pipeline(cfg, depth, np.zeros((2, 2)), np.zeros(2))
+        for i in range(2):
+            ref = oracle_env(cfg, depth[i].numpy(), (0.0, 0.0), 0.0)
+            assert normwise(obs.blurred[i].cpu().numpy(), ref["blurred"]) <= BLUR_TOL
+
+    @pytest.mark.parametrize("hw", [(2, 2), (5, 7), (33, 47), (61, 130)])
+    def test_ragged_sizes(self, hw):
+        """Tiny and non-multiple-of-tile / non-multiple-of-4 frames (scalar load path)."""
+        h, w = hw
+        cfg = small_config(h, w, grid=(3, 4), pitch=synthetic.PITCH * 4)
+        depth = depth_batch(3, h, w, seed=7, pitch=synthetic.PITCH * 4)
+        shear, twist = synthetic.loads(3, 8)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        for i in range(3):
+            check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
+
+    def test_zero_envs(self):
+        cfg = small_config(48, 64)
+        obs = run_pipeline(cfg, torch.zeros((0, 48, 64)), np.zeros((0, 2)), np.zeros(0))
+        assert obs.rgb.shape == (0, 48, 64, 3)
+
+    def test_indentation_input_kind(self):
+        cfg = small_config(48, 64)
+        depth = depth_batch(2, 48, 64, seed=9)
+        ind = torch.clamp(synthetic.REST - depth.double(), 0, synthetic.REST).float()
+        obs = run_pipeline(cfg, ind, np.zeros((2, 2)), np.zeros(2), input_kind="indentation")
+        for i in range(2):
+            ref = oracle_env(cfg, depth[i].numpy(), (0.0, 0.0), 0.0)
+            assert normwise(obs.blurred[i].cpu().numpy(), ref["blurred"]) <= BLUR_TOL
+
+    def test_nonfinite_inputs_counted(self):
+        cfg = small_config(48, 64)
+        depth = torch.full((2, 48, 64), synthetic.REST, dtype=torch.float32)
+        depth[1, 5, 7] = float("nan")
+        depth[1, 40, 60] = float("inf")
+        obs = run_pipeline(cfg, depth, np.zeros((2, 2)), np.zeros(2))
+        assert obs.summary[0, 6].item() == 0
+        assert obs.summary[1, 6].item() == 2
+
+    def test_workspace_reuse_is_deterministic(self):
+        cfg = small_config(48, 64)
+        depth = depth_batch(5, 48, 64, seed=13)
+        shear, twist = synthetic.loads(5, 14)
+        a = run_pipeline(cfg, depth, shear, twist)
+        b = run_pipeline(cfg, depth, shear, twist)
+        assert torch.equal(a.rgb, b.rgb)
+        assert torch.equal(a.disp, b.disp)
+        assert torch.equal(a.summary, b.summary)
+
+    def test_tracked_loads_match_track_load(self):
+        """TAC_LOAD_TRACK: state advanced by pose deltas (REF/marker.py:124-140)."""
+        cfg = small_config(48, 64)
+        n, steps = 4, 5
+        pipe = TactilePipeline(cfg, DEV)
+        state = pipe.new_state(n)
+        ref_state = [dict(cx=0.0, cy=0.0, dmax=0.0, sx=0.0, sy=0.0, twist=0.0, in_contact=False)
+                     for _ in range(n)]
+        rng = np.random.default_rng(17)
+        mp = cfg.marker_params
+        params = (mp.k_n, mp.lambda_n, mp.lambda_s, mp.k_t, mp.lambda_t)
+        for t in range(steps):
+            depth = depth_batch(n, 48, 64, seed=100 + t, fixed_kind="sphere")
+            if t == 2:
+                depth[1] = synthetic.REST  # contact lost for env 1
+            delta = rng.uniform(-1e-4, 1e-4, (n, 3))
+            obs = pipe.simulate(depth.to(DEV), state=state,
+                                pose_delta=torch.as_tensor(delta, device=DEV))
+            torch.cuda.synchronize()
+            for i in range(n):
+                ind = otac.indentation_from(depth[i].numpy().astype(np.float64), synthetic.REST)
+                c = omk.contact_center(ind, cfg.pixel_pitch)
+                ref_state[i] = omk.track_load(ref_state[i], delta[i], c)
+                got = state[i].cpu().numpy()
+                exp = [ref_state[i][k] for k in ("cx", "cy", "dmax", "sx", "sy", "twist")]
+                assert np.allclose(got[:6], exp, rtol=1e-5, atol=1e-9)
+                assert got[6] == float(ref_state[i]["in_contact"])
+                u = omk.marker_displacements(ref_state[i], cfg.rest_grid, params)
+                assert normwise(obs.disp[i].cpu().numpy(), u) <= DISP_TOL
+
+
+class TestMirrorsAgainstReferenceGolden:
+    """The batched mirrors against vectors produced by the reference itself."""
+
+    def test_indentation_from(self, golden):
+        g = golden("tactile")
+        depth = torch.as_tensor(g["depth"], dtype=torch.float32, device=DEV)
+        sensor = SensorConfig.from_pitch(48, 64, float(g["pitch"]), float(g["rest"]))
+        ind = indentation_from(HeightMap(depth, float(g["pitch"])), sensor)
+        d32 = g["depth"].astype(np.float32).astype(np.float64)
+        exp = np.clip(float(g["rest"]) - d32, 0, float(g["rest"]))  # fp64 truth on the fp32 input
+        got = ind.values.cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(got - exp) <= 2.4e-7 * exp + 1e-12)  # <= 1 ulp of fp32
+        assert np.array_equal(got == 0, exp == 0)
+
+    @pytest.mark.parametrize("ki", range(5))
+    def test_smooth_pyramid_kernel_sizes(self, golden, ki):
+        g = golden("tactile")
+        ind = torch.as_tensor(g["ind"], dtype=torch.float32, device=DEV)
+        out = smooth_pyramid(IndentationMap(ind, float(g["pitch"])), g[f"ksizes_{ki}"])
+        ref = g[f"smooth_k{ki}"]
+        for i in range(ref.shape[0]):
+            assert normwise(out.values[i].cpu().numpy(), ref[i]) <= BLUR_TOL
+
+    def test_identity_kernel_bit_exact(self, golden):
+        g = golden("tactile")
+        ind = torch.as_tensor(g["ind"], dtype=torch.float32, device=DEV)
+        out = smooth_pyramid(IndentationMap(ind, float(g["pitch"])), [1])
+        assert torch.equal(out.values, ind)
+
+    @pytest.mark.parametrize("si", range(3))
+    def test_smooth_pyramid_sigmas(self, golden, si):
+        g = golden("tactile")
+        ind = torch.as_tensor(g["ind"], dtype=torch.float32, device=DEV)
+        out = smooth_pyramid(IndentationMap(ind, float(g["pitch"])), sigmas=g[f"sigmas_{si}"])
+        ref = g[f"smooth_s{si}"]
+        for i in range(ref.shape[0]):
+            assert normwise(out.values[i].cpu().numpy(), ref[i]) <= BLUR_TOL
+
+    def test_normals(self, golden):
+        g = golden("optical")
+        sm = torch.as_tensor(g["smooth"], dtype=torch.float32, device=DEV)
+        n = normals_from(IndentationMap(sm, 2.66e-5)).cpu().numpy()
+        assert np.abs(n - g["normals"]).max() < 1e-4
+        tilt = normals_from(torch.as_tensor(g["tilted"], dtype=torch.float32, device=DEV), 2.5e-5)
+        assert np.abs(tilt.cpu().numpy() - g["tilted_normals"]).max() < 1e-6
+
+    def test_single_bin_lut_reproduces_reference_shade(self, golden):
+        from paper_2411_04776_b200 import lut_from_polytable
+
+        g = golden("optical")
+        cfg = PipelineConfig(
+            sensor=SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9)),
+            levels=levels_from_kernel_sizes(),
+            lut=lut_from_polytable(g["coeffs"]),
+            background=(g["background"] * 255.0).astype(np.float32),
+        )
+        sm = torch.as_tensor(g["smooth"], dtype=torch.float32, device=DEV)
+        rgb = shade(sm, cfg).cpu().numpy()
+        mx, frac = rgb_stats(rgb, g["shaded_u8"])
+        assert mx <= 1 and frac >= RGB_FRAC
+
+    def test_contact_center(self, golden):
+        g = golden("marker")
+        sensor = SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9))
+        cfg = marker_config(sensor)
+        maps = torch.as_tensor(g["cc_maps"], dtype=torch.float32, device=DEV)
+        contact, summary = contact_center(maps, cfg)
+        c = contact.cpu().numpy()
+        for i, ref in enumerate(g["cc"]):
+            assert c[i, 6] == ref[3]
+            assert np.allclose(c[i, :3], ref[:3], rtol=1e-5, atol=1e-9)
+
+    def test_two_pixel_centroid(self, golden):
+        g = golden("marker")
+        sensor = SensorConfig.from_pitch(9, 9, 2.66e-5, 4e-3, (3, 3))
+        cfg = marker_config(sensor)
+        two = torch.zeros((1, 9, 9), dtype=torch.float32, device=DEV)
+        two[0, 4, 2] = 1e-4
+        two[0, 4, 6] = 3e-4
+        contact, _ = contact_center(two, cfg)
+        c = contact[0].cpu().numpy()
+        assert np.allclose(c[:3], g["cc_two"][:3], rtol=1e-6, atol=1e-18)
+
+    def test_marker_displacements(self, golden):
+        g = golden("marker")
+        sensor = SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9))
+        cfg = marker_config(sensor, rest_grid=g["grid"])
+        L = g["loads"]
+        loads = np.zeros((len(L), 8))
+        loads[:, :7] = L
+        disp = marker_displacements(torch.as_tensor(loads, device=DEV), cfg).cpu().numpy()
+        for i in range(len(L)):
+            assert normwise(disp[i], g["disps"][i]) <= 1e-6
+
+    def test_pure_shear_centre_exact_and_linear(self, golden):
+        """Acceptance c6 (REF test_acceptance.py:237-264): exact shear at the
+        centre marker, exact linearity in shear, zero load -> zero field."""
+        sensor = SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9))
+        cfg = marker_config(sensor)
+        grid = cfg.rest_grid
+        s = (3.7e-4, -1.2e-4)
+        loads = np.zeros((3, 8))
+        loads[0, :7] = [grid[4, 7, 0], grid[4, 7, 1], 0.0, s[0], s[1], 0.0, 1.0]
+        loads[1, :7] = [grid[4, 7, 0], grid[4, 7, 1], 0.0, 2 * s[0], 2 * s[1], 0.0, 1.0]
+        disp = marker_displacements(torch.as_tensor(loads, device=DEV), cfg).cpu().numpy()
+        assert tuple(disp[0, 4, 7]) == (np.float32(s[0]), np.float32(s[1]))
+        assert not disp[2].any()
+        # linearity holds exactly on the fp64 values; the fp32 outputs inherit it
+        assert np.array_equal(disp[1], 2 * disp[0])
+
+    def test_track_load_sequence(self, golden):
+        g = golden("marker")
+        sensor = SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9))
+        cfg = marker_config(sensor)
+        state = torch.zeros((1, 8), dtype=torch.float64, device=DEV)
+        for inp, ref in zip(g["track_in"], g["track_out"]):
+            contact = torch.zeros((1, 8), dtype=torch.float64, device=DEV)
+            contact[0, 0], contact[0, 1], contact[0, 2], contact[0, 6] = inp[3], inp[4], inp[5], inp[6]
+            delta = torch.as_tensor(inp[None, :3], device=DEV)
+            state = track_load(state, delta, contact, cfg)
+            got = state[0].cpu().numpy()
+            assert np.allclose(got[:7], ref, rtol=1e-12, atol=1e-18)
+
+    def test_render_markers_bit_exact(self, golden):
+        g = golden("marker")
+        o = golden("optical")
+        sensor = SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9))
+        for radius, key, base in (
+            (3, "render_r3", oop.quantize_u8(o["shaded"][0])),
+            (4, "render_r4_grey", np.full((48, 64, 3), 230, np.uint8)),
+        ):
+            cfg = marker_config(sensor, dot_radius=radius, rest_grid=g["grid"])
+            rgb = torch.as_tensor(base[None].copy(), device=DEV)
+            disp = torch.as_tensor(g["render_disp"][None], dtype=torch.float32, device=DEV)
+            # fp32 displacements: centres computed from rest + fp32(disp); the
+            # golden disp is far from .5 ties so rounding agrees
+            render_markers(disp, rgb, cfg)
+            assert np.array_equal(rgb[0].cpu().numpy(), g[key])
+
+
+class TestBoundaryErrors:
+    def test_bad_shapes_raise_invalid_argument(self):
+        cfg = small_config(48, 64)
+        pipe = TactilePipeline(cfg, DEV)
+        with pytest.raises(InvalidArgumentError):
+            pipe.simulate(torch.zeros((2, 48, 63), device=DEV), torch.zeros((2, 2), dtype=torch.float64, device=DEV),
+                          torch.zeros(2, dtype=torch.float64, device=DEV))
+        with pytest.raises(InvalidArgumentError):
+            pipe.simulate(torch.zeros((2, 48, 64), device=DEV))
+
+    def test_even_kernel_rejected(self):
+        with pytest.raises(InvalidArgumentError):
+            smooth_pyramid(IndentationMap(torch.zeros((8, 8), device=DEV), 1e-5), [4])
+
+    def test_negative_indentation_rejected(self):
+        with pytest.raises(InvalidArgumentError):
+            IndentationMap(torch.full((4, 4), -1.0, device=DEV), 1e-5)
+
+    def test_radius_above_max_is_unsupported(self):
+        from paper_2411_04776_b200 import UnsupportedConfigError
+
+        with pytest.raises(UnsupportedConfigError):
+            smooth_pyramid(IndentationMap(torch.zeros((64, 64), device=DEV), 1e-5), [51])
