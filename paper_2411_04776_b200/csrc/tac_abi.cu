@@ -23,7 +23,7 @@ struct tac_ctx {
   double* d_grid = nullptr;
   FrameParams fused, blur, contact;  // per-mode launch templates
   MarkerGeom mg;
-  int max_tiles;
+  int max_tiles;  // max column strips per frame over the modes
 };
 
 namespace {
@@ -52,29 +52,30 @@ int env_int(const char* name, int dflt) {
   return std::atoi(s);
 }
 
-// Fill geometry/pitches of a frame-kernel template for a tile size.
-void plan_tiles(FrameParams& p, int mode, int TX, int TY) {
-  p.TX = std::min(TX, p.W);
-  p.TY = std::min(TY, p.H);
-  p.tiles_x = (p.W + p.TX - 1) / p.TX;
-  p.tiles_y = (p.H + p.TY - 1) / p.TY;
-  const int ring = (mode == kModeFused) ? 1 : 0;
-  const int R = (mode == kModeContact) ? 0 : p.R;
-  p.ring = ring;
-  const int EWm = p.TX + 2 * ring, EHm = p.TY + 2 * ring;
-  const int WWm = EWm + 2 * R;
-  int wp = WWm + K;
-  if ((wp & 1) == 0) ++wp;  // odd pitch: row-strided lanes hit distinct banks
-  p.win_pitch = wp;
-  p.win_rows = EHm + 2 * R + K;
-  int ap = EWm + K;
-  if ((ap & 1) == 0) ++ap;
-  p.acc_pitch = ap;
-  p.acc_rows = EHm;
-  if (mode == kModeContact) {
-    // window only; no vbuf / acc needed
-    p.acc_rows = 0;
+static int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Geometry of the strip-streaming kernel for one mode (see tac_frame.cu).
+void plan_strips(FrameParams& p, int mode, int max_strip) {
+  if (mode == kModeContact) p.R = 0;
+  const int R = p.R;
+  if (p.W <= max_strip + max_strip / 10) {
+    p.strips = 1;
+    p.strip_w = p.W;
+  } else {
+    p.strips = (p.W + max_strip - 1) / max_strip;
+    p.strip_w = round_up((p.W + p.strips - 1) / p.strips, 16);
+    p.strips = (p.W + p.strip_w - 1) / p.strip_w;
   }
+  const int ring = (mode == kModeFused && p.strips > 1) ? 1 : 0;
+  const int ew = p.strip_w + 2 * ring;            // blurred columns
+  const int lw = (p.strips == 1) ? round_up(p.W, 4) : round_up(ew + 2 * R + 6, 4);
+  p.in_pitch = round_up(lw, 4);
+  p.in_rows = RB + 2 * R;
+  int vp = round_up(ew, KH) + 2 * R + 1;
+  if ((vp & 1) == 0) ++vp;  // odd: the H pass reads 16 rows x 2 chunks conflict-free
+  p.v_pitch = vp;
+  p.b_pitch = round_up(ew + 3 + 8, 4);
+  p.stage_bytes = (RB + 1) * p.strip_w * 3;
 }
 
 int free_ctx(tac_ctx* c) {
@@ -103,6 +104,11 @@ int common_checks(const tac_ctx* c, int64_t n_env) {
   if (n_env > (int64_t)0x7fffffff / std::max(1, c->max_tiles))
     return fail(TAC_ERR_UNSUPPORTED, "n_env too large for one launch");
   return check_device(c);
+}
+
+int tma_ok(const FrameParams& p, const void* in) {
+  if (env_int("TAC_NO_TMA", 0)) return 0;
+  return (p.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
 }
 
 void bind_workspace(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) {
@@ -265,21 +271,25 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.bg_u8 = c->d_bg_u8;
   b.mg = mg;
 
-  const int tx = env_int("TAC_TILE_X", 64), ty = env_int("TAC_TILE_Y", 30);
+  const int max_strip = std::max(32, env_int("TAC_MAX_STRIP", 320));
   c->fused = b;
-  plan_tiles(c->fused, kModeFused, tx, ty);
+  plan_strips(c->fused, kModeFused, max_strip);
   c->blur = b;
-  plan_tiles(c->blur, kModeBlur, tx, ty + 2);
+  plan_strips(c->blur, kModeBlur, max_strip);
   c->contact = b;
-  plan_tiles(c->contact, kModeContact, std::max(tx, 64), 32);
-  c->max_tiles = std::max({c->fused.tiles_x * c->fused.tiles_y, c->blur.tiles_x * c->blur.tiles_y,
-                           c->contact.tiles_x * c->contact.tiles_y});
+  plan_strips(c->contact, kModeContact, max_strip);
+  c->max_tiles = std::max({c->fused.strips, c->blur.strips, c->contact.strips});
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
-    if (frame_smem_bytes(p, mode) > 227 * 1024) {
+    if (p.stage_bytes > (int)(RB * p.v_pitch * sizeof(float))) {
       free_ctx(c);
-      return fail(TAC_ERR_UNSUPPORTED, "tile %dx%d with radius %d needs %zu B of shared memory",
-                  p.TX, p.TY, R, frame_smem_bytes(p, mode));
+      return fail(TAC_ERR_UNSUPPORTED, "staging buffer does not fit (strip %d)", p.strip_w);
+    }
+    if (frame_smem_bytes(p) > 227 * 1024) {
+      free_ctx(c);
+      return fail(TAC_ERR_UNSUPPORTED,
+                  "strip of %d columns with radius %d needs %zu B of shared memory (max 227 KB); "
+                  "set TAC_MAX_STRIP lower", p.strip_w, p.R, frame_smem_bytes(p));
     }
   }
   *out = c;
@@ -294,9 +304,7 @@ size_t tac_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   return part + (((size_t)n_env * sizeof(unsigned int) + 255) & ~size_t(255));
 }
 
-int32_t tac_tiles_per_frame(const tac_ctx* c) {
-  return c ? c->fused.tiles_x * c->fused.tiles_y : 0;
-}
+int32_t tac_tiles_per_frame(const tac_ctx* c) { return c ? c->fused.strips : 0; }
 
 int tac_indentation(const tac_ctx* c, const float* depth, float* ind, int64_t n_env, void* stream) {
   int st = common_checks(c, n_env);
@@ -318,6 +326,7 @@ int tac_contact_blur(const tac_ctx* c, const float* in, int32_t input_kind, floa
   if (summary && !workspace) return fail(TAC_ERR_INVALID, "summary needs a workspace");
   FrameParams p = c->blur;
   p.in = in;
+  p.use_tma = tma_ok(p, in);
   p.input_depth = input_kind == TAC_INPUT_DEPTH;
   p.blurred = blurred;
   p.n_env = n_env;
@@ -357,6 +366,7 @@ int tac_contact(const tac_ctx* c, const float* in, int32_t input_kind, double* c
   if (!workspace) return fail(TAC_ERR_INVALID, "tac_contact needs a workspace");
   FrameParams p = c->contact;
   p.in = in;
+  p.use_tma = tma_ok(p, in);
   p.input_depth = input_kind == TAC_INPUT_DEPTH;
   p.n_env = n_env;
   p.finalize = 1;
@@ -412,6 +422,7 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   }
   FrameParams p = c->fused;
   p.in = a->in;
+  p.use_tma = tma_ok(p, a->in);
   p.input_depth = a->input_kind == TAC_INPUT_DEPTH;
   p.rgb = a->rgb;
   p.blurred = a->blurred;

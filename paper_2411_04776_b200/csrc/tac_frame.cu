@@ -1,22 +1,34 @@
-// Frame kernels: kernel (a) gel clamp + multi-scale Gaussian pyramid, fused
-// with kernel (b) gradient -> binned LUT -> background -> uint8, and the
-// per-tile contact reductions of kernel (c); the last CTA of every env runs
-// the marker epilogue (centroid, load, displacements, dot splat).
+// Strip-streaming frame kernel: kernel (a) gel clamp + multi-scale Gaussian
+// pyramid, fused with kernel (b) gradient -> binned LUT -> background ->
+// uint8, plus the contact reductions and marker epilogue of kernel (c).
 //
-// One CTA = one (env, output tile).  Per CTA:
-//   1. load the clamped indentation window (tile + 1-px gradient ring + R halo,
-//      replicate borders = scipy mode="nearest", REF/tactile.py:219-221) into
-//      shared memory with 128-bit loads;
-//   2. per-tile contact partials on the raw indentation (REF/marker.py:109-121);
-//   3. if the window is all zero the blur is exactly 0 and the shaded pixel is
-//      exactly rint(bg): copy the quantised background (exact skip);
-//   4. else, per pyramid level: vertical pass (window -> vbuf) and horizontal
-//      pass (vbuf -> acc, += across levels, 1/L folded into the taps);
-//   5. shading from acc (np.gradient semantics incl. one-sided borders,
-//      REF/optical.py:160) -> LUT bins -> c1..c5 x basis -> + bg -> rint ->
-//      clamp -> staged uint8 tile -> 128-bit stores;
-//   6. publish the tile partial; the last tile of the env (atomic ticket)
-//      reduces the partials in fp64 and runs the marker stage.
+// One CTA (320 threads) owns one column strip of one env's frame (a whole
+// 320-wide frame is one strip) and walks it top to bottom in row blocks of
+// RB = 16 rows:
+//
+//   TMA   cp.async.bulk copies the block's new depth rows (clamped row index =
+//         replicate borders, scipy mode="nearest", REF/tactile.py:219-221)
+//         into the input buffer, issued one block ahead so the copy overlaps
+//         the previous block's horizontal pass and shading;
+//   conv  clamp depth -> indentation in place (REF/tactile.py:193-197), fold
+//         the contact partials of REF/marker.py:109-121 and per-row non-zero
+//         flags into the same pass;
+//   V     per level, one thread per column: 16 outputs x (2r+1) taps from
+//         registers (each smem load feeds up to 16 FFMAs);
+//   H     per level, one thread per (row, 16-column chunk), accumulated over
+//         levels into the blurred ring (1/L folded into the taps);
+//   shade four pixels per thread: np.gradient differences (one-sided on the
+//         borders, REF/optical.py:160), normals, magnitude/direction bins,
+//         c1..c5 x basis (REF/optical.py:82-88, :244), + background,
+//         round-half-even with saturation -> staged uint8 -> 16-B stores.
+//
+// A block whose input window is entirely zero blurs to exactly 0 and shades
+// to exactly rint(background): it skips V/H/shade and copies the quantised
+// background (exact, not an approximation).
+//
+// After the last block the CTA reduces its partials; the env epilogue
+// (centroid, load, displacements, dot splat) runs in the same CTA when the
+// frame is one strip, else in the last strip CTA of the env (atomic ticket).
 #include <cstdio>
 
 #include "tac_internal.cuh"
@@ -27,91 +39,190 @@ namespace tac {
 namespace {
 
 constexpr float kPi = 3.14159265358979323846f;
+constexpr float kHalfPi = 1.57079632679489661923f;
 
 __device__ __forceinline__ float clampf(float v, float lo, float hi) {
   return fminf(fmaxf(v, lo), hi);
 }
 
-// ---------------------------------------------------------------------------
-// Separable passes.  RL is the level radius (compile time, so the tap loop is
-// fully unrolled and every tap weight lives in a register).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
-// First pass (vertical, along rows of the window):
-//   vbuf[r][c] = sum_{t=-RL..RL} wv[|t|] * win[r + R + t][c]
-// for ext rows r in [0, EH) and window columns c in [c_lo, c_hi).
+// ---- TMA (bulk async copy) + mbarrier helpers ------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---- per-CTA geometry -------------------------------------------------------
+struct Geo {
+  long long env;
+  int strip;
+  int x0, x1;    // output columns
+  int bx0, bx1;  // blurred columns (output + gradient ring)
+  int vx0, vx1;  // in-frame vertical-pass columns
+  int lx0, lx1;  // loaded columns (16-B aligned for TMA)
+  int bbase;     // global column of blurred-buffer column 0 (4-aligned)
+  int nblocks;
+};
+
+__device__ __forceinline__ Geo make_geo(const FrameParams& p, int mode) {
+  Geo g;
+  g.env = blockIdx.x / p.strips;
+  g.strip = (int)(blockIdx.x - g.env * p.strips);
+  g.x0 = g.strip * p.strip_w;
+  g.x1 = min(g.x0 + p.strip_w, p.W);
+  const int ring = mode == kModeFused ? 1 : 0;
+  g.bx0 = max(g.x0 - ring, 0);
+  g.bx1 = min(g.x1 + ring, p.W);
+  const int R = mode == kModeContact ? 0 : p.R;
+  g.vx0 = max(g.bx0 - R, 0);
+  g.vx1 = min(g.bx1 + R, p.W);
+  if (p.use_tma) {
+    g.lx0 = g.vx0 & ~3;
+    g.lx1 = min((g.vx1 + 3) & ~3, p.W);
+  } else {
+    g.lx0 = g.vx0;
+    g.lx1 = g.vx1;
+  }
+  g.bbase = g.bx0 & ~3;
+  g.nblocks = (p.H + RB - 1) / RB;
+  return g;
+}
+
+// ---- separable passes ---------------------------------------------------------
+// Vertical: vb[k][c - vb_base] = sum_t wv[|t|] * in[R + k + t][c - lx0], k < RB,
+// for in-frame columns c of [bx0 - RL, bx1 + RL).
 template <int RL>
-__device__ __forceinline__ void vpass(const FrameParams& p, int lvl, const float* __restrict__ win,
-                                      float* __restrict__ vbuf, int EH, int c_lo, int c_hi) {
+__device__ __forceinline__ void vpass(const FrameParams& p, const Geo& g, int lvl,
+                                      const float* __restrict__ inb, float* __restrict__ vb) {
   float w[RL + 1];
 #pragma unroll
   for (int i = 0; i <= RL; ++i) w[i] = p.wv[lvl][i];
-  const int ncols = c_hi - c_lo;
-  const int nchunks = (EH + K - 1) / K;
-  const int items = ncols * nchunks;
-  const int pitch = p.win_pitch;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int chunk = it / ncols;
-    const int c = c_lo + (it - chunk * ncols);
-    const int r0 = chunk * K;
-    const float* src = win + (r0 + p.R - RL) * pitch + c;
-    float acc[K];
+  const int c_lo = max(g.bx0 - RL, 0), c_hi = min(g.bx1 + RL, p.W);
+  const int vb_base = g.bx0 - p.R;
+  const int ip = p.in_pitch, vp = p.v_pitch;
+  for (int c = c_lo + (int)threadIdx.x; c < c_hi; c += kThreads) {
+    const float* src = inb + (p.R - RL) * ip + (c - g.lx0);
+    float acc[RB];
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = 0.f;
+    for (int k = 0; k < RB; ++k) acc[k] = 0.f;
 #pragma unroll
-    for (int j = 0; j < K + 2 * RL; ++j) {
-      const float v = src[j * pitch];
+    for (int j = 0; j < RB + 2 * RL; ++j) {
+      const float v = src[j * ip];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
+      for (int k = 0; k < RB; ++k) {
         const int t = j - k - RL;
         if (t >= -RL && t <= RL) acc[k] = fmaf(w[t < 0 ? -t : t], v, acc[k]);
       }
     }
-    float* dst = vbuf + r0 * pitch + c;
+    float* dst = vb + (c - vb_base);
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (r0 + k < EH) dst[k * pitch] = acc[k];
+    for (int k = 0; k < RB; ++k) dst[k * vp] = acc[k];
   }
 }
 
-// Second pass (horizontal):
-//   acc[r][c] (+)= sum_{t=-RL..RL} wh[|t|] * src[r][c + off + t]
-// for ext rows r in [0, EH), ext cols c in [0, EW).
+// Replicate the vertical-pass result into columns outside the frame (H-pass pads).
+__device__ __forceinline__ void vpad(const FrameParams& p, const Geo& g, int RL, float* vb) {
+  const int left = max(0, RL - g.bx0);         // columns bx0-RL .. -1
+  const int right = max(0, g.bx1 + RL - p.W);  // columns W .. bx1+RL-1
+  const int n = left + right;
+  if (n == 0) return;
+  const int vb_base = g.bx0 - p.R;
+  for (int it = threadIdx.x; it < n * RB; it += kThreads) {
+    const int k = it / n;
+    const int q = it - k * n;
+    float* row = vb + k * p.v_pitch;
+    if (q < left)
+      row[(-1 - q) - vb_base] = row[0 - vb_base];
+    else
+      row[(p.W + (q - left)) - vb_base] = row[(p.W - 1) - vb_base];
+  }
+}
+
+// Horizontal: bb[2 + r][c - bbase] (+)= sum_t wh[|t|] * vb[r][c + t - vb_base]
+// for r < RB, c in [bx0, bx1).  Lanes 0-15 / 16-31 take rows 0-15 of two
+// chunks 16 floats apart: conflict-free with the odd v_pitch.
 template <int RL>
-__device__ __forceinline__ void hpass(const FrameParams& p, int lvl, const float* __restrict__ src_base,
-                                      int src_pitch, int off, float* __restrict__ accb, int EH,
-                                      int EW, bool first) {
+__device__ __forceinline__ void hpass(const FrameParams& p, const Geo& g, int lvl,
+                                      const float* __restrict__ vb, float* __restrict__ bb,
+                                      bool first) {
   float w[RL + 1];
 #pragma unroll
   for (int i = 0; i <= RL; ++i) w[i] = p.wh[lvl][i];
-  const int nchunks = (EW + K - 1) / K;
-  const int items = EH * nchunks;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int chunk = it / EH;
-    const int r = it - chunk * EH;
-    const int c0 = chunk * K;
-    const float* src = src_base + r * src_pitch + c0 + off - RL;
-    float acc[K];
+  const int EW = g.bx1 - g.bx0;
+  const int nchunks = (EW + KH - 1) / KH;
+  const int vb_base = g.bx0 - p.R;
+  for (int it = threadIdx.x; it < nchunks * RB; it += kThreads) {
+    const int r = it & (RB - 1);
+    const int c0 = (it / RB) * KH;
+    const float* src = vb + r * p.v_pitch + (g.bx0 + c0 - RL - vb_base);
+    float acc[KH];
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = 0.f;
+    for (int k = 0; k < KH; ++k) acc[k] = 0.f;
 #pragma unroll
-    for (int j = 0; j < K + 2 * RL; ++j) {
+    for (int j = 0; j < KH + 2 * RL; ++j) {
       const float v = src[j];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
+      for (int k = 0; k < KH; ++k) {
         const int t = j - k - RL;
         if (t >= -RL && t <= RL) acc[k] = fmaf(w[t < 0 ? -t : t], v, acc[k]);
       }
     }
-    float* dst = accb + r * p.acc_pitch + c0;
-    if (first) {
+    float* dst = bb + (2 + r) * p.b_pitch + (g.bx0 + c0 - g.bbase);
+    if (c0 + KH <= EW) {
+      if (first) {
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (c0 + k < EW) dst[k] = acc[k];
+        for (int k = 0; k < KH; ++k) dst[k] = acc[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < KH; ++k) dst[k] += acc[k];
+      }
     } else {
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (c0 + k < EW) dst[k] += acc[k];
+      for (int k = 0; k < KH; ++k)
+        if (c0 + k < EW) dst[k] = first ? acc[k] : dst[k] + acc[k];
     }
+  }
+}
+
+// Identity level (k == 1): bb (+)= in / L, straight from the input buffer.
+__device__ __forceinline__ void ident_level(const FrameParams& p, const Geo& g, int lvl,
+                                            const float* inb, float* bb, bool first) {
+  const float w = p.wh[lvl][0];
+  const int EW = g.bx1 - g.bx0;
+  for (int it = threadIdx.x; it < EW * RB; it += kThreads) {
+    const int r = it / EW;
+    const int c = g.bx0 + (it - r * EW);
+    const float v = w * inb[(p.R + r) * p.in_pitch + (c - g.lx0)];
+    float* d = bb + (2 + r) * p.b_pitch + (c - g.bbase);
+    *d = first ? v : *d + v;
   }
 }
 
@@ -119,109 +230,177 @@ __device__ __forceinline__ void hpass(const FrameParams& p, int lvl, const float
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
   X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24)
 
-// One pyramid level into acc.  Identity levels (radius 0) read the window.
-__device__ __forceinline__ void blur_level(const FrameParams& p, int lvl, const float* win,
-                                           float* vbuf, float* accb, int EH, int EW, bool first) {
-  const int RL = p.radius[lvl];
-  if (RL == 0) {
-    hpass<0>(p, lvl, win + p.R * p.win_pitch, p.win_pitch, p.R, accb, EH, EW, first);
-    __syncthreads();
-    return;
-  }
-  // the horizontal pass reads window columns [R - RL, R + EW + RL)
-  const int c_lo = p.R - RL;
-  const int c_hi = p.R + EW + RL;
-  switch (RL) {
-#define X(r)                                        \
-  case r:                                           \
-    vpass<r>(p, lvl, win, vbuf, EH, c_lo, c_hi);    \
-    break;
-    TAC_RADIUS_CASES(X)
-#undef X
-    default:
-      break;
-  }
-  __syncthreads();
-  switch (RL) {
-#define X(r)                                                                  \
-  case r:                                                                     \
-    hpass<r>(p, lvl, vbuf, p.win_pitch, p.R, accb, EH, EW, first);            \
-    break;
-    TAC_RADIUS_CASES(X)
-#undef X
-    default:
-      break;
-  }
-  __syncthreads();
+// ---- shading ------------------------------------------------------------------
+// atan(a) for a in [0, 1]: odd minimax polynomial, |err| ~ 1e-7 rad in fp32.
+__device__ __forceinline__ float atan01(float a) {
+  const float s = a * a;
+  float q = 0.0024567204527556896f;
+  q = fmaf(q, s, -0.01440134271979332f);
+  q = fmaf(q, s, 0.039781197905540466f);
+  q = fmaf(q, s, -0.07234855741262436f);
+  q = fmaf(q, s, 0.10498945415019989f);
+  q = fmaf(q, s, -0.14161229133605957f);
+  q = fmaf(q, s, 0.19985906779766083f);
+  q = fmaf(q, s, -0.33332598209381104f);
+  q = fmaf(q, s, 0.9999998807907104f);
+  return q * a;
 }
 
-// Copy `nbytes` from shared to global, 16 B at a time when both ends allow.
-__device__ __forceinline__ void store_row_bytes(uint8_t* dst, const uint8_t* src, int nbytes,
-                                                int lane, int nlanes) {
-  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | nbytes) & 15) == 0) {
-    const uint4* s = reinterpret_cast<const uint4*>(src);
-    uint4* d = reinterpret_cast<uint4*>(dst);
-    for (int i = lane; i < nbytes / 16; i += nlanes) d[i] = s[i];
-  } else if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | nbytes) & 3) == 0) {
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
-    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
-    for (int i = lane; i < nbytes / 4; i += nlanes) d[i] = s[i];
-  } else {
-    for (int i = lane; i < nbytes; i += nlanes) dst[i] = src[i];
-  }
+// atan2(y, x) for (x, y) != 0.
+__device__ __forceinline__ float atan2_nz(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  float r = atan01(__fdividef(mn, mx));
+  r = (ay > ax) ? kHalfPi - r : r;
+  r = (x < 0.f) ? kPi - r : r;
+  return (y < 0.f) ? -r : r;
 }
 
-// Shade one pixel from the blurred ext tile (acc).  Returns packed RGB.
-// `b` points at the pixel's blurred value inside a tile of row pitch `bp`.
-__device__ __forceinline__ void shade_px(const FrameParams& p, const float* __restrict__ b, int bp,
-                                         int y, int x, const float* __restrict__ bgp,
-                                         uint8_t* out3) {
-  float gx, gy;
-  // np.gradient: central inside, one-sided first order on the borders
-  if (x == 0)
-    gx = (b[1] - b[0]) * p.inv_p;
-  else if (x == p.W - 1)
-    gx = (b[0] - b[-1]) * p.inv_p;
-  else
-    gx = (b[1] - b[-1]) * p.inv_2p;
-  if (y == 0)
-    gy = (b[bp] - b[0]) * p.inv_p;
-  else if (y == p.H - 1)
-    gy = (b[0] - b[-bp]) * p.inv_p;
-  else
-    gy = (b[bp] - b[-bp]) * p.inv_2p;
+__device__ __forceinline__ uint32_t u8sat(float v) {
+  uint32_t r;
+  asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+
+// Add the binned-LUT shading of gradient (gx, gy) to background (r, g, b).
+__device__ __forceinline__ void shade_one(const FrameParams& p, float gx, float gy, float& r,
+                                          float& g, float& b) {
   const float g2 = fmaf(gx, gx, gy * gy);
-  float r = bgp[0], g = bgp[1], bl = bgp[2];
   if (g2 > 0.f) {
+    const float gm = g2 * rsqrtf(g2);
     const float inv = rsqrtf(1.f + g2);
     const float nx = -gx * inv, ny = -gy * inv;
-    const float gm = sqrtf(g2);
     const int mb = min((int)(gm * p.mag_scale), p.mag_bins - 1);
-    int db = (int)((atan2f(gy, gx) + kPi) * p.dir_scale);
-    if (db >= p.dir_bins) db -= p.dir_bins;
-    if (db < 0) db = 0;
+    int db = (int)((atan2_nz(gy, gx) + kPi) * p.dir_scale);
+    db = db >= p.dir_bins ? db - p.dir_bins : db;
+    db = max(db, 0);
     const float4* L = p.lut + ((long long)mb * p.dir_bins + db) * 4;
     const float4 a = __ldg(L + 0), c = __ldg(L + 1), d = __ldg(L + 2), e = __ldg(L + 3);
     const float nxx = nx * nx, nxy = nx * ny, nyy = ny * ny;
-    // layout: a = R(c1..c4), c = R c5, G c1..c3, d = G c4..c5, B c1..c2, e = B c3..c5, pad
-    const float dR = a.x * nx + a.y * ny + a.z * nxx + a.w * nxy + c.x * nyy;
-    const float dG = c.y * nx + c.z * ny + c.w * nxx + d.x * nxy + d.y * nyy;
-    const float dB = d.z * nx + d.w * ny + e.x * nxx + e.y * nxy + e.z * nyy;
-    r += dR;
-    g += dG;
-    bl += dB;
+    // layout: a = R c1..c4 | c = R c5, G c1..c3 | d = G c4, c5, B c1, c2 | e = B c3..c5, pad
+    r += a.x * nx + a.y * ny + a.z * nxx + a.w * nxy + c.x * nyy;
+    g += c.y * nx + c.z * ny + c.w * nxx + d.x * nxy + d.y * nyy;
+    b += d.z * nx + d.w * ny + e.x * nxx + e.y * nxy + e.z * nyy;
   }
-  out3[0] = (uint8_t)min(max(__float2int_rn(r), 0), 255);
-  out3[1] = (uint8_t)min(max(__float2int_rn(g), 0), 255);
-  out3[2] = (uint8_t)min(max(__float2int_rn(bl), 0), 255);
 }
 
-// Deterministic block reduction of kSumFields values (fields 0..3, 5..7 sum;
-// field 4 max).  Result valid in thread 0.
-__device__ __forceinline__ void block_reduce_partial(float v[kSumFields], float* s_red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// Shade rows [y_lo, y_hi) of the strip into the staging buffer (rows relative
+// to y_lo).  Four consecutive pixels per thread (16-B background loads, 12-B
+// staged stores).
+__device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, int r0, int y_lo,
+                                           int y_hi, const float* __restrict__ bb,
+                                           uint8_t* __restrict__ stage) {
+  const int OW = g.x1 - g.x0;
+  const int ng = (OW + 3) >> 2;
+  const int sw3 = OW * 3;
+  const int rows = y_hi - y_lo;
+  const bool vec_bg = (p.W & 3) == 0;
+  for (int it = threadIdx.x; it < rows * ng; it += kThreads) {
+    const int yy = it / ng;
+    const int gi = it - yy * ng;
+    const int y = y_lo + yy;
+    const int xg = g.x0 + 4 * gi;
+    const float* rc = bb + (y - r0 + 2) * p.b_pitch + (xg - g.bbase);
+    const float* rm = rc - p.b_pitch;
+    const float* rp = rc + p.b_pitch;
+    float c[6], m[4], n[4];
+    c[0] = rc[-1];
 #pragma unroll
-  for (int f = 0; f < kSumFields; ++f) {
+    for (int k = 0; k < 4; ++k) {
+      c[k + 1] = rc[k];
+      m[k] = rm[k];
+      n[k] = rp[k];
+    }
+    c[5] = rc[4];
+    float bgv[12];
+    const float* bgp = p.bg + ((long long)y * p.W + xg) * 3;
+    if (vec_bg && xg + 4 <= g.x1) {
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);
+      const float4 b2 = __ldg(reinterpret_cast<const float4*>(bgp) + 2);
+      bgv[0] = b0.x; bgv[1] = b0.y; bgv[2] = b0.z; bgv[3] = b0.w;
+      bgv[4] = b1.x; bgv[5] = b1.y; bgv[6] = b1.z; bgv[7] = b1.w;
+      bgv[8] = b2.x; bgv[9] = b2.y; bgv[10] = b2.z; bgv[11] = b2.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) bgv[k] = (xg + k / 3 < g.x1) ? __ldg(bgp + k) : 0.f;
+    }
+    const bool top = (y == 0), bot = (y == p.H - 1);
+    const float sy = (top || bot) ? p.inv_p : p.inv_2p;
+    uint32_t q[12];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = xg + k;
+      const bool lft = (x == 0), rgt = (x == p.W - 1);
+      const float xr = rgt ? c[k + 1] : c[k + 2];
+      const float xl = lft ? c[k + 1] : c[k];
+      const float gxv = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
+      const float yb = bot ? c[k + 1] : n[k];
+      const float yt = top ? c[k + 1] : m[k];
+      const float gyv = (yb - yt) * sy;
+      float r = bgv[3 * k], gg = bgv[3 * k + 1], b = bgv[3 * k + 2];
+      shade_one(p, gxv, gyv, r, gg, b);
+      q[3 * k] = u8sat(r);
+      q[3 * k + 1] = u8sat(gg);
+      q[3 * k + 2] = u8sat(b);
+    }
+    uint8_t* dst = stage + yy * sw3 + 4 * gi * 3;
+    if (xg + 4 <= g.x1 && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+      uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+      d32[0] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+      d32[1] = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+      d32[2] = q[8] | (q[9] << 8) | (q[10] << 16) | (q[11] << 24);
+    } else {
+      for (int k = 0; k < 12 && xg + k / 3 < g.x1; ++k) dst[k] = (uint8_t)q[k];
+    }
+  }
+}
+
+// staged rows -> global, one warp per row, 16 B per lane when aligned.
+__device__ __forceinline__ void store_rows(uint8_t* out_rows, long long row_stride,
+                                           const uint8_t* stage, int rows, int nbytes) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+  for (int rr = wid; rr < rows; rr += nw) {
+    uint8_t* dst = out_rows + rr * row_stride;
+    const uint8_t* src = stage + rr * nbytes;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | nbytes;
+    if ((al & 15) == 0) {
+      for (int i = lane; i < nbytes / 16; i += 32)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else if ((al & 3) == 0) {
+      for (int i = lane; i < nbytes / 4; i += 32)
+        reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+    } else {
+      for (int i = lane; i < nbytes; i += 32) dst[i] = src[i];
+    }
+  }
+}
+
+// Copy quantised-background rows (blocks whose blur is exactly zero).
+__device__ __forceinline__ void bg_rows(const FrameParams& p, const Geo& g, uint8_t* out, int y_lo,
+                                        int y_hi) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+  const int nbytes = (g.x1 - g.x0) * 3;
+  for (int y = y_lo + wid; y < y_hi; y += nw) {
+    const long long o = ((long long)y * p.W + g.x0) * 3;
+    uint8_t* d = out + o;
+    const uint8_t* s = p.bg_u8 + o;
+    if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(s) | nbytes) & 15) == 0) {
+      for (int i = lane; i < nbytes / 16; i += 32)
+        reinterpret_cast<uint4*>(d)[i] = __ldg(reinterpret_cast<const uint4*>(s) + i);
+    } else {
+      for (int i = lane; i < nbytes; i += 32) d[i] = s[i];
+    }
+  }
+}
+
+// ---- reductions / epilogue ------------------------------------------------------
+// Fields: 0 count, 1 sum w, 2 sum w*xc, 3 sum w*yc, 4 max, 5 non-finite.
+// Fixed shuffle tree + fixed warp order: deterministic.
+__device__ __forceinline__ void block_reduce(float v[6], float* s_red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float u = __shfl_xor_sync(0xffffffffu, v[f], o);
@@ -230,330 +409,331 @@ __device__ __forceinline__ void block_reduce_partial(float v[kSumFields], float*
   }
   if (lane == 0) {
 #pragma unroll
-    for (int f = 0; f < kSumFields; ++f) s_red[wid * kSumFields + f] = v[f];
+    for (int f = 0; f < 6; ++f) s_red[wid * 8 + f] = v[f];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < nw; ++w) {
 #pragma unroll
-      for (int f = 0; f < kSumFields; ++f) {
-        const float u = s_red[w * kSumFields + f];
+      for (int f = 0; f < 6; ++f) {
+        const float u = s_red[w * 8 + f];
         v[f] = (f == 4) ? fmaxf(v[f], u) : v[f] + u;
       }
     }
   }
 }
 
-// Last CTA of an env: fp64 reduction of the tile partials, contact outputs,
-// load (given or tracked), marker displacements and dot splat.
-__device__ void env_epilogue(const FrameParams& p, long long env, int T, int* s_int,
-                             double* s_dbl) {
-  const float* part = p.partials + env * (long long)T * kSumFields;
-  if (threadIdx.x < 32) {
-    double cnt = 0.0, sw = 0.0, swx = 0.0, swy = 0.0, nf = 0.0;
-    float mx = 0.f;
-    for (int t = threadIdx.x; t < T; t += 32) {
-      const float* q = part + t * kSumFields;
-      cnt += (double)__ldcg(q + 0);
-      sw += (double)__ldcg(q + 1);
-      swx += (double)__ldcg(q + 2);
-      swy += (double)__ldcg(q + 3);
-      mx = fmaxf(mx, __ldcg(q + 4));
-      nf += (double)__ldcg(q + 5);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      sw += __shfl_xor_sync(0xffffffffu, sw, o);
-      swx += __shfl_xor_sync(0xffffffffu, swx, o);
-      swy += __shfl_xor_sync(0xffffffffu, swy, o);
-      nf += __shfl_xor_sync(0xffffffffu, nf, o);
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (threadIdx.x == 0) {
-      const double pitch = p.mg.pitch;
-      Load c = load_zero();
-      if (cnt > 0.0) {
-        c.in_contact = true;
-        c.cx = swx / sw * pitch;
-        c.cy = swy / sw * pitch;
-        c.dmax = (double)mx;
-      }
-      if (p.summary != nullptr) {
-        float* s = p.summary + env * kSumFields;
-        s[0] = c.in_contact ? 1.f : 0.f;
-        s[1] = (float)(cnt * pitch * pitch);
-        s[2] = (float)c.cx;
-        s[3] = (float)c.cy;
-        s[4] = (float)c.dmax;
-        s[5] = c.in_contact ? (float)(sw * pitch * pitch) : 0.f;
-        s[6] = (float)nf;
-        s[7] = 0.f;
-      }
-      if (p.contact != nullptr) load_store(p.contact + env * 8, c);
-      Load l = c;
-      if (p.finalize == 2) {
-        if (p.load_mode == TAC_LOAD_TRACK) {
-          const Load prev = load_from(p.state + env * 8);
-          const double* dl = p.pose_delta + env * 3;
-          l = track_load(prev, dl[0], dl[1], dl[2], c);
-          load_store(p.state + env * 8, l);
-        } else if (c.in_contact) {
-          l.sx = p.shear[2 * env];
-          l.sy = p.shear[2 * env + 1];
-          l.twist = p.twist[env];
-        }
-      }
-      s_dbl[0] = l.cx;
-      s_dbl[1] = l.cy;
-      s_dbl[2] = l.dmax;
-      s_dbl[3] = l.sx;
-      s_dbl[4] = l.sy;
-      s_dbl[5] = l.twist;
-      s_dbl[6] = l.in_contact ? 1.0 : 0.0;
-      // leave the ticket counter zeroed for the next launch
-      p.counters[env] = 0u;
-    }
+// Thread 0: totals (fp64) -> contact outputs + load; the load lands in s_dbl.
+__device__ void finalize_load(const FrameParams& p, long long env, double cnt, double sw, double swx,
+                              double swy, float mx, double nf, double* s_dbl) {
+  const double pitch = p.mg.pitch;
+  Load c = load_zero();
+  if (cnt > 0.0) {
+    c.in_contact = true;
+    c.cx = swx / sw * pitch;
+    c.cy = swy / sw * pitch;
+    c.dmax = (double)mx;
   }
-  __syncthreads();
+  if (p.summary != nullptr) {
+    float* s = p.summary + env * kSumFields;
+    s[0] = c.in_contact ? 1.f : 0.f;
+    s[1] = (float)(cnt * pitch * pitch);
+    s[2] = (float)c.cx;
+    s[3] = (float)c.cy;
+    s[4] = (float)c.dmax;
+    s[5] = c.in_contact ? (float)(sw * pitch * pitch) : 0.f;
+    s[6] = (float)nf;
+    s[7] = 0.f;
+  }
+  if (p.contact != nullptr) load_store(p.contact + env * 8, c);
+  Load l = c;
   if (p.finalize == 2) {
-    const Load l = load_from(s_dbl);
-    const long long HW = (long long)p.H * p.W;
-    const int nm = p.mg.rows * p.mg.cols;
-    markers_block(p.mg, l, p.disp ? p.disp + env * (long long)nm * 2 : nullptr,
-                  p.splat ? p.rgb + env * HW * 3 : nullptr, nullptr, s_int, s_int + nm);
+    if (p.load_mode == TAC_LOAD_TRACK) {
+      const Load prev = load_from(p.state + env * 8);
+      const double* dl = p.pose_delta + env * 3;
+      l = track_load(prev, dl[0], dl[1], dl[2], c);
+      load_store(p.state + env * 8, l);
+    } else if (c.in_contact) {
+      l.sx = p.shear[2 * env];
+      l.sy = p.shear[2 * env + 1];
+      l.twist = p.twist[env];
+    }
   }
+  load_store(s_dbl, l);
+}
+
+__device__ __forceinline__ void shift_halo(const FrameParams& p, float* inb, int LW, int R) {
+  // rows [RB, RB + 2R) -> [0, 2R); each thread owns whole columns and walks
+  // them in increasing row order, so the overlapping copy is safe.
+  for (int c = threadIdx.x; c < LW; c += kThreads)
+    for (int k = 0; k < 2 * R; ++k) inb[k * p.in_pitch + c] = inb[(RB + k) * p.in_pitch + c];
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__ FrameParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int T = p.tiles_x * p.tiles_y;
-  const long long env = blockIdx.x / T;
-  const int tile = blockIdx.x - (int)(env * T);
-  const int ty = tile / p.tiles_x, tx = tile - ty * p.tiles_x;
-  const int x0 = tx * p.TX, y0 = ty * p.TY;
-  const int x1 = min(x0 + p.TX, p.W), y1 = min(y0 + p.TY, p.H);
-  const int ring = (MODE == kModeFused) ? 1 : 0;
-  const int ex0 = max(x0 - ring, 0), ex1 = min(x1 + ring, p.W);
-  const int ey0 = max(y0 - ring, 0), ey1 = min(y1 + ring, p.H);
-  const int EW = ex1 - ex0, EH = ey1 - ey0;
-  const int R = (MODE == kModeContact) ? 0 : p.R;
-  const int WW = EW + 2 * R, WH = EH + 2 * R;
+__global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constant__ FrameParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Geo g = make_geo(p, MODE);
+  const int R = MODE == kModeContact ? 0 : p.R;
   const long long HW = (long long)p.H * p.W;
+  const int tid = threadIdx.x;
 
-  float* win = reinterpret_cast<float*>(smem_raw);
-  float* vbuf = win + p.win_rows * p.win_pitch;
-  float* accb = vbuf + p.win_rows * p.win_pitch;
-  float* s_red = accb + p.acc_rows * p.acc_pitch;  // 8 warps x 8
-  int* s_int = reinterpret_cast<int*>(s_red + (kThreads / 32) * kSumFields);
-  __shared__ int s_flag;
+  float* inb = reinterpret_cast<float*>(smem_raw);
+  float* vb = inb + p.in_rows * p.in_pitch;
+  float* bb = vb + RB * p.v_pitch;
+  // RB + 2 rows + 1 spare row: the last image row reads its (unused) lower
+  // neighbour one row past the ring
+  float* s_red = bb + (RB + 3) * p.b_pitch;  // 10 warps x 8
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_red + (kThreads / 32) * 8);
+  unsigned char* rownz = reinterpret_cast<unsigned char*>(bar + 1);  // index: global row + R
+  int* s_int = reinterpret_cast<int*>(rownz + ((p.H + 2 * p.R + RB + 15) & ~15));
   __shared__ double s_dbl[8];
+  __shared__ int s_flag;
+  uint8_t* stage = reinterpret_cast<uint8_t*>(vb);
 
-  // ---- 1. clamped indentation window (replicate borders) -------------------
-  const float* src = p.in + env * HW;
-  const int gx0 = ex0 - R;  // global col of window col 0
-  const int gy0 = ey0 - R;  // global row of window row 0
-  // in-frame column span of the window
-  const int cx_lo = max(gx0, 0), cx_hi = min(gx0 + WW, p.W);
-  float nonfinite = 0.f;
-  const bool vec = ((p.W & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  if (vec) {
-    const int a_lo = cx_lo & ~3;             // aligned start
-    const int a_hi = (cx_hi + 3) & ~3;       // aligned end (<= W since W % 4 == 0)
-    const int nv = (a_hi - a_lo) >> 2;
-    const int items = WH * nv;
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int wr = it / nv;
-      const int v4 = it - wr * nv;
-      const int gy = min(max(gy0 + wr, 0), p.H - 1);
-      const int gc = a_lo + 4 * v4;
-      const float4 d = __ldg(reinterpret_cast<const float4*>(src + (long long)gy * p.W + gc));
-      const float dv[4] = {d.x, d.y, d.z, d.w};
-      const bool own_row = (gy0 + wr >= y0) && (gy0 + wr < y1);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int g = gc + q;
-        if (g < cx_lo || g >= cx_hi) continue;
-        float v = dv[q];
-        if (own_row && g >= x0 && g < x1 && !isfinite(v)) nonfinite += 1.f;
-        if (p.input_depth) v = clampf((p.rest - v) + p.rest_lo, 0.f, p.rest);
-        win[wr * p.win_pitch + (g - gx0)] = v;
+  const float* src = p.in + g.env * HW;
+  const int LW = g.lx1 - g.lx0;
+  const unsigned row_bytes = (unsigned)LW * 4u;
+
+  // rows [ga, gb) (global, unclamped) -> buffer rows starting at `slot`
+  auto issue_rows = [&](int ga, int gb, int slot) {
+    if (p.use_tma) {
+      if (tid == 0) {
+        mbar_expect_tx(bar, row_bytes * (unsigned)(gb - ga));
+        for (int gr = ga; gr < gb; ++gr) {
+          const int cr = min(max(gr, 0), p.H - 1);
+          bulk_g2s(inb + (slot + gr - ga) * p.in_pitch, src + (long long)cr * p.W + g.lx0, row_bytes,
+                   bar);
+        }
+      }
+    } else {
+      for (int it = tid; it < (gb - ga) * LW; it += kThreads) {
+        const int rr = it / LW;
+        const int cc = it - rr * LW;
+        const int cr = min(max(ga + rr, 0), p.H - 1);
+        inb[(slot + rr) * p.in_pitch + cc] = src[(long long)cr * p.W + g.lx0 + cc];
       }
     }
-  } else {
-    const int nc = cx_hi - cx_lo;
-    const int items = WH * nc;
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int wr = it / nc;
-      const int g = cx_lo + (it - wr * nc);
-      const int gy = min(max(gy0 + wr, 0), p.H - 1);
-      float v = src[(long long)gy * p.W + g];
-      const bool own = (gy0 + wr >= y0) && (gy0 + wr < y1) && g >= x0 && g < x1;
-      if (own && !isfinite(v)) nonfinite += 1.f;
-      if (p.input_depth) v = clampf((p.rest - v) + p.rest_lo, 0.f, p.rest);
-      win[wr * p.win_pitch + (g - gx0)] = v;
-    }
+  };
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = tid; i < p.H + 2 * p.R + RB; i += kThreads) rownz[i] = 0;
   __syncthreads();
-  // replicate columns that fall outside the frame
-  if (gx0 < 0 || gx0 + WW > p.W) {
-    const int left = cx_lo - gx0;            // window cols [0, left) copy col `left`
-    const int right = cx_hi - gx0;           // window cols [right, WW) copy col right-1
-    const int npad = left + (WW - right);
-    for (int it = threadIdx.x; it < WH * npad; it += blockDim.x) {
-      const int wr = it / npad;
-      const int k = it - wr * npad;
-      float* row = win + wr * p.win_pitch;
-      if (k < left)
-        row[k] = row[left];
-      else
-        row[right + (k - left)] = row[right - 1];
+
+  float red[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  unsigned phase = 0;
+  issue_rows(-R, RB + R, 0);  // block 0 window
+
+  uint8_t* out = (MODE == kModeFused) ? p.rgb + g.env * HW * 3 : nullptr;
+
+  for (int b = 0; b < g.nblocks; ++b) {
+    const int r0 = b * RB;
+    const bool last = (b == g.nblocks - 1);
+    // ---- wait for this block's rows, convert the new ones -------------------
+    if (p.use_tma) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+      __syncthreads();
+    }
+    {
+      const int ga = (b == 0) ? r0 - R : r0 + R;  // first new global row
+      const int slot = (b == 0) ? 0 : 2 * R;
+      const int nrows = (b == 0) ? RB + 2 * R : RB;
+      const int c_lo = g.vx0 - g.lx0, c_hi = g.vx1 - g.lx0;
+      for (int it = tid; it < nrows * LW; it += kThreads) {
+        const int rr = it / LW;
+        const int cc = it - rr * LW;
+        const int gr = ga + rr;
+        float* e = inb + (slot + rr) * p.in_pitch + cc;
+        float v = *e;
+        const int gx = g.lx0 + cc;
+        const bool own = gr >= 0 && gr < p.H && gx >= g.x0 && gx < g.x1;
+        if (own && !isfinite(v)) red[5] += 1.f;
+        if (p.input_depth) v = clampf((p.rest - v) + p.rest_lo, 0.f, p.rest);
+        *e = v;
+        if (own) {
+          red[4] = fmaxf(red[4], v);
+          if (v > p.threshold) {
+            red[0] += 1.f;
+            red[1] += v;
+            red[2] = fmaf(v, (float)gx + 0.5f - p.half_w, red[2]);
+            red[3] = fmaf(v, (float)gr + 0.5f - p.half_h, red[3]);
+          }
+        }
+        if (v != 0.f && cc >= c_lo && cc < c_hi) rownz[gr + p.R] = 1;
+      }
+    }
+    __syncthreads();
+
+    if (MODE == kModeContact) {
+      if (!last) {
+        fence_proxy_async();
+        __syncthreads();
+        issue_rows(r0 + RB, r0 + 2 * RB, 0);
+      }
+      continue;
+    }
+
+    // ---- blur ------------------------------------------------------------------
+    int any = 0;
+    for (int i = tid; i < RB + 2 * R; i += kThreads) any |= rownz[r0 + i];  // rows r0-R .. r0+RB+R-1
+    any = __syncthreads_or(any);
+    if (any) {
+      for (int l = 0; l < p.n_levels; ++l) {
+        const int RL = p.radius[l];
+        const bool lastl = (l == p.n_levels - 1);
+        if (RL == 0) {
+          ident_level(p, g, l, inb, bb, l == 0);
+        } else {
+          switch (RL) {
+#define X(r)                    \
+  case r:                       \
+    vpass<r>(p, g, l, inb, vb); \
+    break;
+            TAC_RADIUS_CASES(X)
+#undef X
+            default:
+              break;
+          }
+        }
+        __syncthreads();
+        if (lastl && !last) {
+          // this block's input rows are consumed: shift the halo, then start
+          // the next block's copy (overlaps the H pass and the shading)
+          shift_halo(p, inb, LW, R);
+          fence_proxy_async();
+        }
+        if (RL > 0) vpad(p, g, RL, vb);
+        __syncthreads();
+        if (lastl && !last) issue_rows(r0 + RB + R, r0 + 2 * RB + R, 2 * R);
+        if (RL > 0) {
+          switch (RL) {
+#define X(r)                            \
+  case r:                               \
+    hpass<r>(p, g, l, vb, bb, l == 0);  \
+    break;
+            TAC_RADIUS_CASES(X)
+#undef X
+            default:
+              break;
+          }
+        }
+        __syncthreads();
+      }
+    } else {
+      // exact zero: the blurred rows are 0
+      for (int it = tid; it < RB * p.b_pitch; it += kThreads) bb[2 * p.b_pitch + it] = 0.f;
+      if (!last) {
+        shift_halo(p, inb, LW, R);
+        fence_proxy_async();
+      }
+      __syncthreads();
+      if (!last) issue_rows(r0 + RB + R, r0 + 2 * RB + R, 2 * R);
+    }
+
+    // ---- outputs ---------------------------------------------------------------
+    if (p.blurred != nullptr) {
+      float* dst = p.blurred + g.env * HW;
+      const int OW = g.x1 - g.x0;
+      const int nr = min(RB, p.H - r0);
+      for (int it = tid; it < nr * OW; it += kThreads) {
+        const int rr = it / OW;
+        const int x = g.x0 + (it - rr * OW);
+        dst[(long long)(r0 + rr) * p.W + x] = bb[(2 + rr) * p.b_pitch + (x - g.bbase)];
+      }
+    }
+    if (MODE == kModeFused) {
+      const int y_lo = max(r0 - 1, 0);
+      const int y_hi = last ? p.H : r0 + RB - 1;
+      // blurred rows y-1..y+1 of every shaded row are exactly zero iff input
+      // rows [y_lo-1-R, y_hi+R] are zero
+      int nz = 0;
+      for (int i = tid; i < (y_hi - y_lo) + 2 + 2 * p.R; i += kThreads) {
+        const int gr = y_lo - 1 - p.R + i;
+        if (gr >= -p.R && gr < p.H + p.R) nz |= rownz[gr + p.R];
+      }
+      nz = __syncthreads_or(nz);
+      if (nz) {
+        shade_rows(p, g, r0, y_lo, y_hi, bb, stage);
+        __syncthreads();
+        store_rows(out + ((long long)y_lo * p.W + g.x0) * 3, (long long)p.W * 3, stage, y_hi - y_lo,
+                   (g.x1 - g.x0) * 3);
+      } else {
+        bg_rows(p, g, out, y_lo, y_hi);
+      }
+      __syncthreads();
+      // keep blurred rows r0+RB-2, r0+RB-1 for the next block's gradient
+      for (int it = tid; it < 2 * p.b_pitch; it += kThreads) bb[it] = bb[RB * p.b_pitch + it];
     }
     __syncthreads();
   }
 
-  // ---- 2. per-tile contact partials on the raw indentation -----------------
-  float part[kSumFields];
-#pragma unroll
-  for (int f = 0; f < kSumFields; ++f) part[f] = 0.f;
-  part[5] = nonfinite;
-  int any = 0;
-  {
-    const int tw = x1 - x0, th = y1 - y0;
-    for (int it = threadIdx.x; it < tw * th; it += blockDim.x) {
-      const int yy = it / tw;
-      const int xx = it - yy * tw;
-      const float v = win[(y0 + yy - gy0) * p.win_pitch + (x0 + xx - gx0)];
-      part[4] = fmaxf(part[4], v);
-      if (v > p.threshold) {
-        const float xc = (float)(x0 + xx) + 0.5f - p.half_w;
-        const float yc = (float)(y0 + yy) + 0.5f - p.half_h;
-        part[0] += 1.f;
-        part[1] += v;
-        part[2] = fmaf(v, xc, part[2]);
-        part[3] = fmaf(v, yc, part[3]);
-      }
-    }
-    if (MODE != kModeContact) {
-      for (int it = threadIdx.x; it < WH * WW; it += blockDim.x) {
-        const int wr = it / WW;
-        const int wc = it - wr * WW;
-        if (win[wr * p.win_pitch + wc] != 0.f) {
-          any = 1;
-          break;
-        }
-      }
-    }
-  }
-  if (MODE != kModeContact) any = __syncthreads_or(any);
-
-  // ---- 3/4. blur ------------------------------------------------------------
-  if (MODE != kModeContact && any) {
-    for (int l = 0; l < p.n_levels; ++l) blur_level(p, l, win, vbuf, accb, EH, EW, l == 0);
-  }
-
-  if (MODE == kModeBlur && p.blurred != nullptr) {
-    float* dst = p.blurred + env * HW;
-    const int tw = x1 - x0, th = y1 - y0;
-    for (int it = threadIdx.x; it < tw * th; it += blockDim.x) {
-      const int yy = it / tw;
-      const int xx = it - yy * tw;
-      dst[(long long)(y0 + yy) * p.W + x0 + xx] =
-          any ? accb[(y0 + yy - ey0) * p.acc_pitch + (x0 + xx - ex0)] : 0.f;
-    }
-  }
-
-  // ---- 5. shading -------------------------------------------------------------
-  if (MODE == kModeFused) {
-    const int tw = x1 - x0, th = y1 - y0;
-    uint8_t* stage = reinterpret_cast<uint8_t*>(vbuf);  // vbuf is dead now
-    uint8_t* out = p.rgb + env * HW * 3;
-    if (any) {
-      if (p.blurred != nullptr) {
-        float* dst = p.blurred + env * HW;
-        for (int it = threadIdx.x; it < tw * th; it += blockDim.x) {
-          const int yy = it / tw;
-          const int xx = it - yy * tw;
-          dst[(long long)(y0 + yy) * p.W + x0 + xx] =
-              accb[(y0 + yy - ey0) * p.acc_pitch + (x0 + xx - ex0)];
-        }
-      }
-      for (int it = threadIdx.x; it < tw * th; it += blockDim.x) {
-        const int yy = it / tw;
-        const int xx = it - yy * tw;
-        const int y = y0 + yy, x = x0 + xx;
-        shade_px(p, accb + (y - ey0) * p.acc_pitch + (x - ex0), p.acc_pitch, y, x,
-                 p.bg + ((long long)y * p.W + x) * 3, stage + (yy * tw + xx) * 3);
-      }
-      __syncthreads();
-      // rows of 3*tw bytes -> global, one warp per row
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      for (int yy = wid; yy < th; yy += nw)
-        store_row_bytes(out + ((long long)(y0 + yy) * p.W + x0) * 3, stage + yy * tw * 3, tw * 3,
-                        lane, 32);
-    } else {
-      if (p.blurred != nullptr) {
-        float* dst = p.blurred + env * HW;
-        for (int it = threadIdx.x; it < tw * th; it += blockDim.x) {
-          const int yy = it / tw;
-          dst[(long long)(y0 + yy) * p.W + x0 + (it - yy * tw)] = 0.f;
-        }
-      }
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      for (int yy = wid; yy < th; yy += nw) {
-        const long long o = ((long long)(y0 + yy) * p.W + x0) * 3;
-        uint8_t* d = out + o;
-        const uint8_t* s = p.bg_u8 + o;
-        if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(s) | (tw * 3)) & 15) == 0) {
-          for (int i = lane; i < tw * 3 / 16; i += 32)
-            reinterpret_cast<uint4*>(d)[i] = __ldg(reinterpret_cast<const uint4*>(s) + i);
-        } else {
-          for (int i = lane; i < tw * 3; i += 32) d[i] = s[i];
-        }
-      }
-    }
-  }
-
-  // ---- 6. publish partial, last tile of the env runs the epilogue ------------
+  // ---- reduction + env epilogue -------------------------------------------------
   if (p.finalize == 0) return;
-  block_reduce_partial(part, s_red);
-  if (threadIdx.x == 0) {
-    float* q = p.partials + (env * T + tile) * kSumFields;
-#pragma unroll
-    for (int f = 0; f < kSumFields; ++f) q[f] = part[f];
+  block_reduce(red, s_red);
+  if (p.strips == 1) {
+    if (tid == 0) finalize_load(p, g.env, red[0], red[1], red[2], red[3], red[4], red[5], s_dbl);
+  } else {
+    if (tid == 0) {
+      float* q = p.partials + (g.env * p.strips + g.strip) * kSumFields;
+      for (int f = 0; f < 6; ++f) q[f] = red[f];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned ticket = atomicAdd(p.counters + g.env, 1u);
+      s_flag = ticket == (unsigned)(p.strips - 1);
+    }
+    __syncthreads();
+    if (!s_flag) return;
+    __threadfence();
+    if (tid == 0) {
+      double cnt = 0, sw = 0, swx = 0, swy = 0, nf = 0;
+      float mx = 0.f;
+      const float* q = p.partials + g.env * p.strips * kSumFields;
+      for (int s = 0; s < p.strips; ++s) {  // fixed order: deterministic
+        cnt += __ldcg(q + s * 8 + 0);
+        sw += __ldcg(q + s * 8 + 1);
+        swx += __ldcg(q + s * 8 + 2);
+        swy += __ldcg(q + s * 8 + 3);
+        mx = fmaxf(mx, __ldcg(q + s * 8 + 4));
+        nf += __ldcg(q + s * 8 + 5);
+      }
+      finalize_load(p, g.env, cnt, sw, swx, swy, mx, nf, s_dbl);
+      p.counters[g.env] = 0u;
+    }
   }
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int ticket = atomicAdd(p.counters + env, 1u);
-    s_flag = (ticket == (unsigned int)(T - 1));
+  if (p.finalize == 2) {
+    const Load l = load_from(s_dbl);
+    const int nm = p.mg.rows * p.mg.cols;
+    markers_block(p.mg, l, p.disp ? p.disp + g.env * (long long)nm * 2 : nullptr,
+                  p.splat ? p.rgb + g.env * HW * 3 : nullptr, nullptr, s_int, s_int + nm);
   }
-  __syncthreads();
-  if (!s_flag) return;
-  __threadfence();
-  env_epilogue(p, env, T, s_int, s_dbl);
 }
 
-size_t frame_smem_bytes(const FrameParams& p, int mode) {
-  size_t floats = 2 * (size_t)p.win_rows * p.win_pitch + (size_t)p.acc_rows * p.acc_pitch +
-                  (kThreads / 32) * kSumFields;
-  size_t bytes = floats * sizeof(float);
+size_t frame_smem_bytes(const FrameParams& p) {
+  size_t bytes = sizeof(float) * ((size_t)p.in_rows * p.in_pitch + (size_t)RB * p.v_pitch +
+                                  (size_t)(RB + 3) * p.b_pitch + (kThreads / 32) * 8);
+  bytes += sizeof(uint64_t);
+  bytes += (p.H + 2 * p.R + RB + 15) & ~15;
   bytes += 2 * sizeof(int) * (size_t)p.mg.rows * p.mg.cols;
-  (void)mode;
-  return (bytes + 15) & ~size_t(15);
+  return (bytes + 127) & ~size_t(127);
 }
 
 template <int MODE>
 static cudaError_t launch_mode(const FrameParams& p, cudaStream_t s) {
-  const size_t smem = frame_smem_bytes(p, MODE);
+  const size_t smem = frame_smem_bytes(p);
   cudaError_t e = cudaFuncSetAttribute(frame_kernel<MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long blocks = p.n_env * (long long)(p.tiles_x * p.tiles_y);
+  const long long blocks = p.n_env * (long long)p.strips;
   if (blocks == 0) return cudaSuccess;
   frame_kernel<MODE><<<(unsigned)blocks, kThreads, smem, s>>>(p);
   return cudaGetLastError();
@@ -572,7 +752,7 @@ cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// Stand-alone shade (kernel (b) from a blurred map in HBM).
+// Stand-alone shade (kernel (b) from a blurred map in HBM), one pixel per thread.
 __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ FrameParams p,
                                                     const float* __restrict__ blurred,
                                                     uint8_t* __restrict__ rgb) {
@@ -582,22 +762,20 @@ __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ Fram
   const long long env = i / HW;
   const int pix = (int)(i - env * HW);
   const int y = pix / p.W, x = pix - y * p.W;
-  // gather the 3x3 neighbourhood into a tiny local tile so shade_px applies
-  float loc[9];
   const float* b = blurred + env * HW;
-#pragma unroll
-  for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int yy = min(max(y + dy, 0), p.H - 1), xx = min(max(x + dx, 0), p.W - 1);
-      loc[(dy + 1) * 3 + (dx + 1)] = __ldg(b + (long long)yy * p.W + xx);
-    }
-  uint8_t o[3];
-  shade_px(p, loc + 4, 3, y, x, p.bg + (long long)pix * 3, o);
+  const int xl = x > 0 ? x - 1 : x, xr = x < p.W - 1 ? x + 1 : x;
+  const int yt = y > 0 ? y - 1 : y, yb = y < p.H - 1 ? y + 1 : y;
+  const float gx = (__ldg(b + y * p.W + xr) - __ldg(b + y * p.W + xl)) *
+                   ((xr - xl == 2) ? p.inv_2p : p.inv_p);
+  const float gy = (__ldg(b + yb * p.W + x) - __ldg(b + yt * p.W + x)) *
+                   ((yb - yt == 2) ? p.inv_2p : p.inv_p);
+  const float* bgp = p.bg + (long long)pix * 3;
+  float r = bgp[0], g = bgp[1], bl = bgp[2];
+  shade_one(p, gx, gy, r, g, bl);
   uint8_t* d = rgb + i * 3;
-  d[0] = o[0];
-  d[1] = o[1];
-  d[2] = o[2];
+  d[0] = (uint8_t)u8sat(r);
+  d[1] = (uint8_t)u8sat(g);
+  d[2] = (uint8_t)u8sat(bl);
 }
 
 cudaError_t launch_shade(const FrameParams& p, const float* blurred, uint8_t* rgb, long long n_env,

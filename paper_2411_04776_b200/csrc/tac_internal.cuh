@@ -8,12 +8,11 @@
 
 namespace tac {
 
-// Register-blocking factor of the separable passes: each thread produces K
-// consecutive outputs along the pass direction, so every shared-memory load
-// feeds up to K FFMAs.
-constexpr int K = 8;
-constexpr int kThreads = 256;
-constexpr int kSumFields = 8;  // per-tile partial / per-env summary width
+// Strip-streaming frame kernel geometry (see tac_frame.cu).
+constexpr int RB = 16;        // rows per row block (vertical-pass register block)
+constexpr int KH = 16;        // horizontal-pass outputs per thread
+constexpr int kThreads = 320; // threads per CTA (= 320 columns of a 320-wide strip)
+constexpr int kSumFields = 8; // per-strip partial / per-env summary width
 
 // Frame-kernel modes.
 enum FrameMode : int {
@@ -37,21 +36,22 @@ struct MarkerGeom {
 struct FrameParams {
   // geometry
   int H, W;
-  int TX, TY;            // output tile
-  int tiles_x, tiles_y;  // tiles per frame = tiles_x * tiles_y
-  int R;                 // max radius over levels (window halo)
-  int ring;              // 1 when shading is fused (gradient needs +-1), else 0
-  int win_pitch, acc_pitch;  // smem pitches (floats); vbuf uses win_pitch
-  int win_rows;          // allocated window rows (incl. K pad rows)
-  int acc_rows;
+  int strips;            // column strips per frame (CTAs per env)
+  int strip_w;           // output columns per strip (multiple of 16 unless W is smaller)
+  int R;                 // max radius over levels (vertical halo rows)
+  int in_rows, in_pitch; // input buffer: in_rows x in_pitch floats
+  int v_pitch;           // vertical-pass buffer: RB x v_pitch floats (odd pitch)
+  int b_pitch;           // blurred ring: (RB + 2 (+1 spare)) x b_pitch floats (multiple of 4)
+  int stage_bytes;       // uint8 RGB staging (aliases the vertical-pass buffer)
+  int use_tma;           // rows 16-B aligned -> cp.async.bulk row loads
   // pyramid
   int n_levels;
   int radius[TAC_MAX_LEVELS];
-  float wv[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // first (vertical) pass taps, centre first
-  float wh[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // second (horizontal) pass taps, folded with 1/L
+  float wv[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // vertical taps, centre first
+  float wh[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // horizontal taps, folded with 1/L
   // clamp / contact
-  float rest;           // gel thickness rounded to fp32
-  float rest_lo;        // rest - (double)rest: the clamp runs in ~fp64 accuracy
+  float rest;            // gel thickness rounded to fp32
+  float rest_lo;         // rest - (double)rest: the clamp runs in ~fp64 accuracy
   float threshold;
   float half_w, half_h;  // W/2, H/2 (pixel-centre coordinates)
   // shading
@@ -67,10 +67,10 @@ struct FrameParams {
   int input_depth;
   float* blurred;        // nullable
   uint8_t* rgb;          // fused mode
-  float* partials;       // workspace [N][T][8]
+  float* partials;       // workspace [N][strips][8]
   unsigned int* counters;// workspace [N]
   long long n_env;
-  // finalize (last CTA of an env)
+  // finalize
   int finalize;          // 0 none, 1 contact/summary, 2 + markers
   float* summary;        // nullable [N][8]
   double* contact;       // nullable [N][8] fp64 LoadState
@@ -85,7 +85,7 @@ struct FrameParams {
   int splat;
 };
 
-size_t frame_smem_bytes(const FrameParams& p, int mode);
+size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,
                                cudaStream_t s);
@@ -99,6 +99,5 @@ cudaError_t launch_marker_displacements(const MarkerGeom& m, const double* loads
                                         float* disp, long long n_env, cudaStream_t s);
 cudaError_t launch_render_markers(const MarkerGeom& m, const float* disp, uint8_t* rgb,
                                   long long n_env, cudaStream_t s);
-cudaError_t launch_quantize_bg(const float* bg, uint8_t* bg_u8, long long n, cudaStream_t s);
 
 }  // namespace tac
