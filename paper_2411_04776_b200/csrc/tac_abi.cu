@@ -67,14 +67,17 @@ void plan_strips(FrameParams& p, int mode, int max_strip) {
     p.strips = (p.W + p.strip_w - 1) / p.strip_w;
   }
   const int ring = (mode == kModeFused && p.strips > 1) ? 1 : 0;
-  const int ew = p.strip_w + 2 * ring;            // blurred columns
+  const int ew = p.strip_w + 2 * ring + 3;        // blurred columns (origin 4-aligned)
   const int lw = (p.strips == 1) ? round_up(p.W, 4) : round_up(ew + 2 * R + 6, 4);
   p.in_pitch = round_up(lw, 4);
   p.in_rows = RB + 2 * R;
   int vp = round_up(ew, KH) + 2 * R + 1;
   if ((vp & 1) == 0) ++vp;  // odd: the H pass reads 16 rows x 2 chunks conflict-free
   p.v_pitch = vp;
-  p.b_pitch = round_up(ew + 3 + 8, 4);
+  int bp = round_up(ew + 3 + 8, 4);
+  if (((bp / 4) & 1) == 0) bp += 4;  // 4 x odd: float4 rows on distinct bank groups
+  p.b_pitch = bp;
+  (void)0;
   p.stage_bytes = (RB + 1) * p.strip_w * 3;
 }
 
@@ -112,8 +115,8 @@ int tma_ok(const FrameParams& p, const void* in) {
 }
 
 void bind_workspace(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) {
-  p.partials = reinterpret_cast<float*>(ws);
-  const size_t part_bytes = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(float)) + 255) & ~size_t(255);
+  p.partials = reinterpret_cast<double*>(ws);
+  const size_t part_bytes = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(double)) + 255) & ~size_t(255);
   p.counters = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + part_bytes);
 }
 
@@ -300,7 +303,7 @@ int tac_ctx_destroy(tac_ctx* ctx) { return free_ctx(ctx); }
 
 size_t tac_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   if (!c || n_env < 0) return 0;
-  const size_t part = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(float)) + 255) & ~size_t(255);
+  const size_t part = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(double)) + 255) & ~size_t(255);
   return part + (((size_t)n_env * sizeof(unsigned int) + 255) & ~size_t(255));
 }
 

@@ -99,7 +99,7 @@ __device__ __forceinline__ Geo make_geo(const FrameParams& p, int mode) {
   g.x0 = g.strip * p.strip_w;
   g.x1 = min(g.x0 + p.strip_w, p.W);
   const int ring = mode == kModeFused ? 1 : 0;
-  g.bx0 = max(g.x0 - ring, 0);
+  g.bx0 = max(g.x0 - ring, 0) & ~3;  // 4-aligned: float4 access to the blurred ring
   g.bx1 = min(g.x1 + ring, p.W);
   const int R = mode == kModeContact ? 0 : p.R;
   g.vx0 = max(g.bx0 - R, 0);
@@ -197,12 +197,20 @@ __device__ __forceinline__ void hpass(const FrameParams& p, const Geo& g, int lv
     }
     float* dst = bb + (2 + r) * p.b_pitch + (g.bx0 + c0 - g.bbase);
     if (c0 + KH <= EW) {
-      if (first) {
+      // 16-B stores: b_pitch = 4 x odd, so 8 consecutive rows hit 8 distinct
+      // 16-B bank groups (conflict-free)
+      float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-        for (int k = 0; k < KH; ++k) dst[k] = acc[k];
-      } else {
-#pragma unroll
-        for (int k = 0; k < KH; ++k) dst[k] += acc[k];
+      for (int q = 0; q < KH / 4; ++q) {
+        float4 o = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        if (!first) {
+          const float4 a = d4[q];
+          o.x += a.x;
+          o.y += a.y;
+          o.z += a.z;
+          o.w += a.w;
+        }
+        d4[q] = o;
       }
     } else {
 #pragma unroll
@@ -262,31 +270,49 @@ __device__ __forceinline__ uint32_t u8sat(float v) {
   return r;
 }
 
+// Bins + normal of one pixel.  Branch-free: a zero gradient gives bin 0 and
+// a zero basis, so its shading term is exactly 0 (the LUT is finite).
+struct Px {
+  const float4* lut;
+  float nx, ny;
+};
+
+__device__ __forceinline__ Px bin_px(const FrameParams& p, float gx, float gy) {
+  const float g2 = fmaf(gx, gx, gy * gy);
+  Px o;
+  const float gm = g2 * rsqrtf(g2);        // NaN for g2 == 0 -> bin 0
+  const float inv = rsqrtf(1.f + g2);
+  o.nx = -gx * inv;
+  o.ny = -gy * inv;
+  const int mb = min((int)(gm * p.mag_scale), p.mag_bins - 1);
+  int db = (int)((atan2_nz(gy, gx) + kPi) * p.dir_scale);  // NaN for (0,0) -> 0
+  db = db >= p.dir_bins ? db - p.dir_bins : db;
+  db = max(db, 0);
+  o.lut = p.lut + ((long long)max(mb, 0) * p.dir_bins + db) * 4;
+  return o;
+}
+
+// Delta_c = c1 nx + c2 ny + c3 nx^2 + c4 nx ny + c5 ny^2 (REF/optical.py:82-88, :244)
+// layout: a = R c1..c4 | c = R c5, G c1..c3 | d = G c4, c5, B c1, c2 | e = B c3..c5, pad
+__device__ __forceinline__ void add_lut(const float4 a, const float4 c, const float4 d, const float4 e,
+                                        float nx, float ny, float& r, float& g, float& b) {
+  const float nxx = nx * nx, nxy = nx * ny, nyy = ny * ny;
+  r += a.x * nx + a.y * ny + a.z * nxx + a.w * nxy + c.x * nyy;
+  g += c.y * nx + c.z * ny + c.w * nxx + d.x * nxy + d.y * nyy;
+  b += d.z * nx + d.w * ny + e.x * nxx + e.y * nxy + e.z * nyy;
+}
+
 // Add the binned-LUT shading of gradient (gx, gy) to background (r, g, b).
 __device__ __forceinline__ void shade_one(const FrameParams& p, float gx, float gy, float& r,
                                           float& g, float& b) {
-  const float g2 = fmaf(gx, gx, gy * gy);
-  if (g2 > 0.f) {
-    const float gm = g2 * rsqrtf(g2);
-    const float inv = rsqrtf(1.f + g2);
-    const float nx = -gx * inv, ny = -gy * inv;
-    const int mb = min((int)(gm * p.mag_scale), p.mag_bins - 1);
-    int db = (int)((atan2_nz(gy, gx) + kPi) * p.dir_scale);
-    db = db >= p.dir_bins ? db - p.dir_bins : db;
-    db = max(db, 0);
-    const float4* L = p.lut + ((long long)mb * p.dir_bins + db) * 4;
-    const float4 a = __ldg(L + 0), c = __ldg(L + 1), d = __ldg(L + 2), e = __ldg(L + 3);
-    const float nxx = nx * nx, nxy = nx * ny, nyy = ny * ny;
-    // layout: a = R c1..c4 | c = R c5, G c1..c3 | d = G c4, c5, B c1, c2 | e = B c3..c5, pad
-    r += a.x * nx + a.y * ny + a.z * nxx + a.w * nxy + c.x * nyy;
-    g += c.y * nx + c.z * ny + c.w * nxx + d.x * nxy + d.y * nyy;
-    b += d.z * nx + d.w * ny + e.x * nxx + e.y * nxy + e.z * nyy;
-  }
+  const Px q = bin_px(p, gx, gy);
+  add_lut(__ldg(q.lut), __ldg(q.lut + 1), __ldg(q.lut + 2), __ldg(q.lut + 3), q.nx, q.ny, r, g, b);
 }
 
 // Shade rows [y_lo, y_hi) of the strip into the staging buffer (rows relative
-// to y_lo).  Four consecutive pixels per thread (16-B background loads, 12-B
-// staged stores).
+// to y_lo).  Four consecutive pixels per thread: float4 reads of the blurred
+// ring (conflict-free), x-neighbours by warp shuffle, 16-B background loads,
+// LUT gathers issued two pixels at a time, 12-B staged stores.
 __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, int r0, int y_lo,
                                            int y_hi, const float* __restrict__ bb,
                                            uint8_t* __restrict__ stage) {
@@ -294,27 +320,32 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
   const int ng = (OW + 3) >> 2;
   const int sw3 = OW * 3;
   const int rows = y_hi - y_lo;
-  const bool vec_bg = (p.W & 3) == 0;
-  for (int it = threadIdx.x; it < rows * ng; it += kThreads) {
-    const int yy = it / ng;
-    const int gi = it - yy * ng;
-    const int y = y_lo + yy;
-    const int xg = g.x0 + 4 * gi;
+  const int step = kThreads / ng;  // rows per sweep (>= 1: strips are <= 4 * kThreads wide)
+  const int gi = threadIdx.x % ng;
+  const int ro = threadIdx.x / ng;
+  const int lane = threadIdx.x & 31;
+  const int xg = g.x0 + 4 * gi;
+  const bool full = xg + 4 <= g.x1;
+  const bool vec_bg = ((p.W & 3) == 0) && full;
+  const bool need_l = (lane == 0) || (gi == 0);
+  const bool need_r = (lane == 31) || (gi == ng - 1);
+  const int x_last = p.W - 1;
+  for (int y0 = 0; y0 < rows; y0 += step) {
+    const int yy = y0 + ro;
+    const bool act = (ro < step) && (yy < rows);
+    const int y = y_lo + (act ? yy : 0);
     const float* rc = bb + (y - r0 + 2) * p.b_pitch + (xg - g.bbase);
-    const float* rm = rc - p.b_pitch;
-    const float* rp = rc + p.b_pitch;
-    float c[6], m[4], n[4];
-    c[0] = rc[-1];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      c[k + 1] = rc[k];
-      m[k] = rm[k];
-      n[k] = rp[k];
-    }
-    c[5] = rc[4];
+    const float4 cc = *reinterpret_cast<const float4*>(rc);
+    const float4 mm = *reinterpret_cast<const float4*>(rc - p.b_pitch);
+    const float4 nn = *reinterpret_cast<const float4*>(rc + p.b_pitch);
+    float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
+    float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
+    if (!act) continue;
+    if (need_l) left = rc[-1];
+    if (need_r) right = rc[4];
     float bgv[12];
     const float* bgp = p.bg + ((long long)y * p.W + xg) * 3;
-    if (vec_bg && xg + 4 <= g.x1) {
+    if (vec_bg) {
       const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
       const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);
       const float4 b2 = __ldg(reinterpret_cast<const float4*>(bgp) + 2);
@@ -325,27 +356,45 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
 #pragma unroll
       for (int k = 0; k < 12; ++k) bgv[k] = (xg + k / 3 < g.x1) ? __ldg(bgp + k) : 0.f;
     }
+    const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
+    const float m[4] = {mm.x, mm.y, mm.z, mm.w};
+    const float n[4] = {nn.x, nn.y, nn.z, nn.w};
     const bool top = (y == 0), bot = (y == p.H - 1);
     const float sy = (top || bot) ? p.inv_p : p.inv_2p;
-    uint32_t q[12];
+    float gxs[4], gys[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int x = xg + k;
-      const bool lft = (x == 0), rgt = (x == p.W - 1);
+      const bool lft = (x == 0), rgt = (x == x_last);
       const float xr = rgt ? c[k + 1] : c[k + 2];
       const float xl = lft ? c[k + 1] : c[k];
-      const float gxv = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
+      gxs[k] = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
       const float yb = bot ? c[k + 1] : n[k];
       const float yt = top ? c[k + 1] : m[k];
-      const float gyv = (yb - yt) * sy;
-      float r = bgv[3 * k], gg = bgv[3 * k + 1], b = bgv[3 * k + 2];
-      shade_one(p, gxv, gyv, r, gg, b);
-      q[3 * k] = u8sat(r);
-      q[3 * k + 1] = u8sat(gg);
-      q[3 * k + 2] = u8sat(b);
+      gys[k] = (yb - yt) * sy;
+    }
+    uint32_t q[12];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const Px p0 = bin_px(p, gxs[2 * h], gys[2 * h]);
+      const Px p1 = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
+      const float4 a0 = __ldg(p0.lut), c0 = __ldg(p0.lut + 1), d0 = __ldg(p0.lut + 2), e0 = __ldg(p0.lut + 3);
+      const float4 a1 = __ldg(p1.lut), c1 = __ldg(p1.lut + 1), d1 = __ldg(p1.lut + 2), e1 = __ldg(p1.lut + 3);
+      float r = bgv[6 * h], gg = bgv[6 * h + 1], b = bgv[6 * h + 2];
+      add_lut(a0, c0, d0, e0, p0.nx, p0.ny, r, gg, b);
+      q[6 * h] = u8sat(r);
+      q[6 * h + 1] = u8sat(gg);
+      q[6 * h + 2] = u8sat(b);
+      r = bgv[6 * h + 3];
+      gg = bgv[6 * h + 4];
+      b = bgv[6 * h + 5];
+      add_lut(a1, c1, d1, e1, p1.nx, p1.ny, r, gg, b);
+      q[6 * h + 3] = u8sat(r);
+      q[6 * h + 4] = u8sat(gg);
+      q[6 * h + 5] = u8sat(b);
     }
     uint8_t* dst = stage + yy * sw3 + 4 * gi * 3;
-    if (xg + 4 <= g.x1 && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+    if (full && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
       uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
       d32[0] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
       d32[1] = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
@@ -395,30 +444,54 @@ __device__ __forceinline__ void bg_rows(const FrameParams& p, const Geo& g, uint
 }
 
 // ---- reductions / epilogue ------------------------------------------------------
-// Fields: 0 count, 1 sum w, 2 sum w*xc, 3 sum w*yc, 4 max, 5 non-finite.
-// Fixed shuffle tree + fixed warp order: deterministic.
-__device__ __forceinline__ void block_reduce(float v[6], float* s_red) {
+// Contact partials.  The first moments are accumulated in fp64: every
+// product w*xc of an fp32 weight and a half-integer pixel coordinate is exact
+// in fp64, so symmetric contacts cancel exactly (a centred flat press gives a
+// centroid of exactly 0, as the fp64 reference does) and the dot centres do
+// not flip on the .5 ties of REF/marker.py:221-225.
+struct Red {
+  float cnt, mx, nf;
+  double sw, swx, swy;
+};
+
+__device__ __forceinline__ Red red_zero() {
+  Red r;
+  r.cnt = r.mx = r.nf = 0.f;
+  r.sw = r.swx = r.swy = 0.0;
+  return r;
+}
+
+// Fixed shuffle tree + fixed warp order: deterministic.  Result in thread 0.
+__device__ __forceinline__ void block_reduce(Red& v, double* s_red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
 #pragma unroll
-  for (int f = 0; f < 6; ++f) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float u = __shfl_xor_sync(0xffffffffu, v[f], o);
-      v[f] = (f == 4) ? fmaxf(v[f], u) : v[f] + u;
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    v.cnt += __shfl_xor_sync(0xffffffffu, v.cnt, o);
+    v.mx = fmaxf(v.mx, __shfl_xor_sync(0xffffffffu, v.mx, o));
+    v.nf += __shfl_xor_sync(0xffffffffu, v.nf, o);
+    v.sw += __shfl_xor_sync(0xffffffffu, v.sw, o);
+    v.swx += __shfl_xor_sync(0xffffffffu, v.swx, o);
+    v.swy += __shfl_xor_sync(0xffffffffu, v.swy, o);
   }
   if (lane == 0) {
-#pragma unroll
-    for (int f = 0; f < 6; ++f) s_red[wid * 8 + f] = v[f];
+    double* q = s_red + wid * 8;
+    q[0] = v.cnt;
+    q[1] = v.sw;
+    q[2] = v.swx;
+    q[3] = v.swy;
+    q[4] = v.mx;
+    q[5] = v.nf;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < nw; ++w) {
-#pragma unroll
-      for (int f = 0; f < 6; ++f) {
-        const float u = s_red[w * 8 + f];
-        v[f] = (f == 4) ? fmaxf(v[f], u) : v[f] + u;
-      }
+      const double* q = s_red + w * 8;
+      v.cnt += (float)q[0];
+      v.sw += q[1];
+      v.swx += q[2];
+      v.swy += q[3];
+      v.mx = fmaxf(v.mx, (float)q[4]);
+      v.nf += (float)q[5];
     }
   }
 }
@@ -469,6 +542,59 @@ __device__ __forceinline__ void shift_halo(const FrameParams& p, float* inb, int
     for (int k = 0; k < 2 * R; ++k) inb[k * p.in_pitch + c] = inb[(RB + k) * p.in_pitch + c];
 }
 
+// Depth -> indentation in place for one float4 group of one row, folding the
+// contact partials (own pixels only) and the row non-zero flag.
+__device__ __forceinline__ void convert4(const FrameParams& p, const Geo& g, float* row, int gr, int cg,
+                                         const bool cown[4], const double cxc[4], const bool cvr[4],
+                                         unsigned char* rownz, Red& red) {
+  float4* e = reinterpret_cast<float4*>(row) + cg;
+  float4 v4 = *e;
+  float v[4] = {v4.x, v4.y, v4.z, v4.w};
+  const bool rown = gr >= 0 && gr < p.H;
+  const double yc = (double)gr + 0.5 - (double)p.half_h;
+  bool nz = false;
+  double rowsum = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool own = rown && cown[q];
+    if (own && !(fabsf(v[q]) < INFINITY)) red.nf += 1.f;
+    if (p.input_depth) v[q] = clampf((p.rest - v[q]) + p.rest_lo, 0.f, p.rest);
+    if (own) {
+      red.mx = fmaxf(red.mx, v[q]);
+      const bool in = v[q] > p.threshold;
+      const double m = in ? (double)v[q] : 0.0;
+      red.cnt += in ? 1.f : 0.f;
+      rowsum += m;
+      red.swx = fma(m, cxc[q], red.swx);
+    }
+    nz |= (v[q] != 0.f) && cvr[q];
+  }
+  red.sw += rowsum;
+  red.swy = fma(rowsum, yc, red.swy);
+  *e = make_float4(v[0], v[1], v[2], v[3]);
+  if (nz) rownz[gr + p.R] = 1;
+}
+
+// Scalar fallback (rows not 16-B aligned).
+__device__ __forceinline__ void convert1(const FrameParams& p, const Geo& g, float* e, int gr, int gx,
+                                         unsigned char* rownz, Red& red) {
+  float v = *e;
+  const bool own = gr >= 0 && gr < p.H && gx >= g.x0 && gx < g.x1;
+  if (own && !(fabsf(v) < INFINITY)) red.nf += 1.f;
+  if (p.input_depth) v = clampf((p.rest - v) + p.rest_lo, 0.f, p.rest);
+  *e = v;
+  if (own) {
+    red.mx = fmaxf(red.mx, v);
+    if (v > p.threshold) {
+      red.cnt += 1.f;
+      red.sw += (double)v;
+      red.swx = fma((double)v, (double)gx + 0.5 - (double)p.half_w, red.swx);
+      red.swy = fma((double)v, (double)gr + 0.5 - (double)p.half_h, red.swy);
+    }
+  }
+  if (v != 0.f && gx >= g.vx0 && gx < g.vx1) rownz[gr + p.R] = 1;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -485,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
   float* bb = vb + RB * p.v_pitch;
   // RB + 2 rows + 1 spare row: the last image row reads its (unused) lower
   // neighbour one row past the ring
-  float* s_red = bb + (RB + 3) * p.b_pitch;  // 10 warps x 8
+  double* s_red = reinterpret_cast<double*>(bb + (RB + 3) * p.b_pitch);  // 10 warps x 8
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_red + (kThreads / 32) * 8);
   unsigned char* rownz = reinterpret_cast<unsigned char*>(bar + 1);  // index: global row + R
   int* s_int = reinterpret_cast<int*>(rownz + ((p.H + 2 * p.R + RB + 15) & ~15));
@@ -525,11 +651,27 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
   for (int i = tid; i < p.H + 2 * p.R + RB; i += kThreads) rownz[i] = 0;
   __syncthreads();
 
-  float red[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  Red red = red_zero();
   unsigned phase = 0;
   issue_rows(-R, RB + R, 0);  // block 0 window
 
   uint8_t* out = (MODE == kModeFused) ? p.rgb + g.env * HW * 3 : nullptr;
+
+  // conversion mapping: thread -> fixed float4 column group, rows strided
+  const int ng4 = LW >> 2;
+  const bool vec_conv = ((LW & 3) == 0) && ng4 > 0 && ng4 <= kThreads;
+  const int cg = vec_conv ? tid % ng4 : 0;
+  const int cro = vec_conv ? tid / ng4 : 0;
+  const int cstep = vec_conv ? kThreads / ng4 : 1;
+  bool cown[4], cvr[4];
+  double cxc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int gx = g.lx0 + 4 * cg + q;
+    cown[q] = gx >= g.x0 && gx < g.x1;
+    cvr[q] = gx >= g.vx0 && gx < g.vx1;
+    cxc[q] = (double)gx + 0.5 - (double)p.half_w;
+  }
 
   for (int b = 0; b < g.nblocks; ++b) {
     const int r0 = b * RB;
@@ -545,28 +687,16 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
       const int ga = (b == 0) ? r0 - R : r0 + R;  // first new global row
       const int slot = (b == 0) ? 0 : 2 * R;
       const int nrows = (b == 0) ? RB + 2 * R : RB;
-      const int c_lo = g.vx0 - g.lx0, c_hi = g.vx1 - g.lx0;
-      for (int it = tid; it < nrows * LW; it += kThreads) {
-        const int rr = it / LW;
-        const int cc = it - rr * LW;
-        const int gr = ga + rr;
-        float* e = inb + (slot + rr) * p.in_pitch + cc;
-        float v = *e;
-        const int gx = g.lx0 + cc;
-        const bool own = gr >= 0 && gr < p.H && gx >= g.x0 && gx < g.x1;
-        if (own && !isfinite(v)) red[5] += 1.f;
-        if (p.input_depth) v = clampf((p.rest - v) + p.rest_lo, 0.f, p.rest);
-        *e = v;
-        if (own) {
-          red[4] = fmaxf(red[4], v);
-          if (v > p.threshold) {
-            red[0] += 1.f;
-            red[1] += v;
-            red[2] = fmaf(v, (float)gx + 0.5f - p.half_w, red[2]);
-            red[3] = fmaf(v, (float)gr + 0.5f - p.half_h, red[3]);
-          }
+      if (vec_conv) {
+        // threads past the last full sweep (cro >= cstep) would duplicate rows
+        for (int rr = cro; cro < cstep && rr < nrows; rr += cstep) convert4(p, g, inb + (slot + rr) * p.in_pitch, ga + rr,
+                                                          cg, cown, cxc, cvr, rownz, red);
+      } else {
+        for (int it = tid; it < nrows * LW; it += kThreads) {
+          const int rr = it / LW;
+          const int cc = it - rr * LW;
+          convert1(p, g, inb + (slot + rr) * p.in_pitch + cc, ga + rr, g.lx0 + cc, rownz, red);
         }
-        if (v != 0.f && cc >= c_lo && cc < c_hi) rownz[gr + p.R] = 1;
       }
     }
     __syncthreads();
@@ -678,11 +808,16 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
   if (p.finalize == 0) return;
   block_reduce(red, s_red);
   if (p.strips == 1) {
-    if (tid == 0) finalize_load(p, g.env, red[0], red[1], red[2], red[3], red[4], red[5], s_dbl);
+    if (tid == 0) finalize_load(p, g.env, red.cnt, red.sw, red.swx, red.swy, red.mx, red.nf, s_dbl);
   } else {
     if (tid == 0) {
-      float* q = p.partials + (g.env * p.strips + g.strip) * kSumFields;
-      for (int f = 0; f < 6; ++f) q[f] = red[f];
+      double* q = p.partials + (g.env * p.strips + g.strip) * kSumFields;
+      q[0] = red.cnt;
+      q[1] = red.sw;
+      q[2] = red.swx;
+      q[3] = red.swy;
+      q[4] = red.mx;
+      q[5] = red.nf;
     }
     __threadfence();
     __syncthreads();
@@ -696,13 +831,13 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
     if (tid == 0) {
       double cnt = 0, sw = 0, swx = 0, swy = 0, nf = 0;
       float mx = 0.f;
-      const float* q = p.partials + g.env * p.strips * kSumFields;
+      const double* q = p.partials + g.env * p.strips * kSumFields;
       for (int s = 0; s < p.strips; ++s) {  // fixed order: deterministic
         cnt += __ldcg(q + s * 8 + 0);
         sw += __ldcg(q + s * 8 + 1);
         swx += __ldcg(q + s * 8 + 2);
         swy += __ldcg(q + s * 8 + 3);
-        mx = fmaxf(mx, __ldcg(q + s * 8 + 4));
+        mx = fmaxf(mx, (float)__ldcg(q + s * 8 + 4));
         nf += __ldcg(q + s * 8 + 5);
       }
       finalize_load(p, g.env, cnt, sw, swx, swy, mx, nf, s_dbl);
@@ -720,7 +855,8 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
 
 size_t frame_smem_bytes(const FrameParams& p) {
   size_t bytes = sizeof(float) * ((size_t)p.in_rows * p.in_pitch + (size_t)RB * p.v_pitch +
-                                  (size_t)(RB + 3) * p.b_pitch + (kThreads / 32) * 8);
+                                  (size_t)(RB + 3) * p.b_pitch) +
+                 sizeof(double) * (kThreads / 32) * 8;
   bytes += sizeof(uint64_t);
   bytes += (p.H + 2 * p.R + RB + 15) & ~15;
   bytes += 2 * sizeof(int) * (size_t)p.mg.rows * p.mg.cols;

@@ -67,7 +67,7 @@ struct FrameParams {
   int input_depth;
   float* blurred;        // nullable
   uint8_t* rgb;          // fused mode
-  float* partials;       // workspace [N][strips][8]
+  double* partials;      // workspace [N][strips][8]
   unsigned int* counters;// workspace [N]
   long long n_env;
   // finalize
