@@ -117,34 +117,53 @@ __device__ __forceinline__ Geo make_geo(const FrameParams& p, int mode) {
 }
 
 // ---- separable passes ---------------------------------------------------------
+// Paired fp32 FMA (FFMA2 on sm_100a): two independent lanes of work per issue.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
 // Vertical: vb[k][c - vb_base] = sum_t wv[|t|] * in[R + k + t][c - lx0], k < RB,
-// for in-frame columns c of [bx0 - RL, bx1 + RL).
+// for in-frame columns c of [bx0 - RL, bx1 + RL).  One item = a column pair x
+// 8 rows (FFMA2 over the pair, LDS.64 loads); consecutive lanes take
+// consecutive pairs, so loads are conflict-free and every load feeds 8 FFMA2.
 template <int RL>
 __device__ __forceinline__ void vpass(const FrameParams& p, const Geo& g, int lvl,
                                       const float* __restrict__ inb, float* __restrict__ vb) {
-  float w[RL + 1];
+  float2 w[RL + 1];
 #pragma unroll
-  for (int i = 0; i <= RL; ++i) w[i] = p.wv[lvl][i];
-  const int c_lo = max(g.bx0 - RL, 0), c_hi = min(g.bx1 + RL, p.W);
+  for (int i = 0; i <= RL; ++i) w[i] = make_float2(p.wv[lvl][i], p.wv[lvl][i]);
+  const int c_lo = max(g.bx0 - RL, 0) & ~1;
+  const int c_hi = (min(g.bx1 + RL, p.W) + 1) & ~1;
+  const int npairs = (c_hi - c_lo) >> 1;
   const int vb_base = g.bx0 - p.R;
   const int ip = p.in_pitch, vp = p.v_pitch;
-  for (int c = c_lo + (int)threadIdx.x; c < c_hi; c += kThreads) {
-    const float* src = inb + (p.R - RL) * ip + (c - g.lx0);
-    float acc[RB];
+  for (int it = threadIdx.x; it < 2 * npairs; it += kThreads) {
+    const int h = it >= npairs ? 1 : 0;
+    const int c = c_lo + 2 * (it - h * npairs);
+    const float* src = inb + (p.R - RL + 8 * h) * ip + (c - g.lx0);
+    float2 acc[8];
 #pragma unroll
-    for (int k = 0; k < RB; ++k) acc[k] = 0.f;
+    for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int j = 0; j < RB + 2 * RL; ++j) {
-      const float v = src[j * ip];
+    for (int j = 0; j < 8 + 2 * RL; ++j) {
+      const float2 v = *reinterpret_cast<const float2*>(src + j * ip);
 #pragma unroll
-      for (int k = 0; k < RB; ++k) {
+      for (int k = 0; k < 8; ++k) {
         const int t = j - k - RL;
-        if (t >= -RL && t <= RL) acc[k] = fmaf(w[t < 0 ? -t : t], v, acc[k]);
+        if (t >= -RL && t <= RL) acc[k] = ffma2(w[t < 0 ? -t : t], v, acc[k]);
       }
     }
-    float* dst = vb + (c - vb_base);
+    float* dst = vb + 8 * h * vp + (c - vb_base);
 #pragma unroll
-    for (int k = 0; k < RB; ++k) dst[k * vp] = acc[k];
+    for (int k = 0; k < 8; ++k) {
+      dst[k * vp] = acc[k].x;
+      dst[k * vp + 1] = acc[k].y;
+    }
   }
 }
 
@@ -156,8 +175,8 @@ __device__ __forceinline__ void vpad(const FrameParams& p, const Geo& g, int RL,
   if (n == 0) return;
   const int vb_base = g.bx0 - p.R;
   for (int it = threadIdx.x; it < n * RB; it += kThreads) {
-    const int k = it / n;
-    const int q = it - k * n;
+    const int k = it & (RB - 1);
+    const int q = it / RB;
     float* row = vb + k * p.v_pitch;
     if (q < left)
       row[(-1 - q) - vb_base] = row[0 - vb_base];
@@ -167,55 +186,61 @@ __device__ __forceinline__ void vpad(const FrameParams& p, const Geo& g, int RL,
 }
 
 // Horizontal: bb[2 + r][c - bbase] (+)= sum_t wh[|t|] * vb[r][c + t - vb_base]
-// for r < RB, c in [bx0, bx1).  Lanes 0-15 / 16-31 take rows 0-15 of two
-// chunks 16 floats apart: conflict-free with the odd v_pitch.
+// for r < RB, c in [bx0, bx1).  One item = rows (r, r + 8) x 8 columns: FFMA2
+// pairs the two rows.  A warp covers 8 row pairs x 4 chunks, conflict-free
+// with the odd v_pitch; results go out as float4 (b_pitch = 4 x odd).
 template <int RL>
 __device__ __forceinline__ void hpass(const FrameParams& p, const Geo& g, int lvl,
                                       const float* __restrict__ vb, float* __restrict__ bb,
                                       bool first) {
-  float w[RL + 1];
+  float2 w[RL + 1];
 #pragma unroll
-  for (int i = 0; i <= RL; ++i) w[i] = p.wh[lvl][i];
+  for (int i = 0; i <= RL; ++i) w[i] = make_float2(p.wh[lvl][i], p.wh[lvl][i]);
   const int EW = g.bx1 - g.bx0;
-  const int nchunks = (EW + KH - 1) / KH;
+  const int nch = (EW + 7) >> 3;
   const int vb_base = g.bx0 - p.R;
-  for (int it = threadIdx.x; it < nchunks * RB; it += kThreads) {
-    const int r = it & (RB - 1);
-    const int c0 = (it / RB) * KH;
-    const float* src = vb + r * p.v_pitch + (g.bx0 + c0 - RL - vb_base);
-    float acc[KH];
+  const int vp = p.v_pitch;
+  for (int it = threadIdx.x; it < 8 * nch; it += kThreads) {
+    const int rp = it & 7;
+    const int c0 = (it >> 3) * 8;
+    const float* s0 = vb + rp * vp + (g.bx0 + c0 - RL - vb_base);
+    const float* s1 = s0 + 8 * vp;
+    float2 acc[8];
 #pragma unroll
-    for (int k = 0; k < KH; ++k) acc[k] = 0.f;
+    for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int j = 0; j < KH + 2 * RL; ++j) {
-      const float v = src[j];
+    for (int j = 0; j < 8 + 2 * RL; ++j) {
+      const float2 v = make_float2(s0[j], s1[j]);
 #pragma unroll
-      for (int k = 0; k < KH; ++k) {
+      for (int k = 0; k < 8; ++k) {
         const int t = j - k - RL;
-        if (t >= -RL && t <= RL) acc[k] = fmaf(w[t < 0 ? -t : t], v, acc[k]);
+        if (t >= -RL && t <= RL) acc[k] = ffma2(w[t < 0 ? -t : t], v, acc[k]);
       }
     }
-    float* dst = bb + (2 + r) * p.b_pitch + (g.bx0 + c0 - g.bbase);
-    if (c0 + KH <= EW) {
-      // 16-B stores: b_pitch = 4 x odd, so 8 consecutive rows hit 8 distinct
-      // 16-B bank groups (conflict-free)
-      float4* d4 = reinterpret_cast<float4*>(dst);
+    float* d0 = bb + (2 + rp) * p.b_pitch + (g.bx0 + c0 - g.bbase);
+    float* d1 = d0 + 8 * p.b_pitch;
+    if (c0 + 8 <= EW) {
+      float4* a4 = reinterpret_cast<float4*>(d0);
+      float4* b4 = reinterpret_cast<float4*>(d1);
 #pragma unroll
-      for (int q = 0; q < KH / 4; ++q) {
-        float4 o = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      for (int q = 0; q < 2; ++q) {
+        float4 o0 = make_float4(acc[4 * q].x, acc[4 * q + 1].x, acc[4 * q + 2].x, acc[4 * q + 3].x);
+        float4 o1 = make_float4(acc[4 * q].y, acc[4 * q + 1].y, acc[4 * q + 2].y, acc[4 * q + 3].y);
         if (!first) {
-          const float4 a = d4[q];
-          o.x += a.x;
-          o.y += a.y;
-          o.z += a.z;
-          o.w += a.w;
+          const float4 x0 = a4[q], x1 = b4[q];
+          o0.x += x0.x; o0.y += x0.y; o0.z += x0.z; o0.w += x0.w;
+          o1.x += x1.x; o1.y += x1.y; o1.z += x1.z; o1.w += x1.w;
         }
-        d4[q] = o;
+        a4[q] = o0;
+        b4[q] = o1;
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < KH; ++k)
-        if (c0 + k < EW) dst[k] = first ? acc[k] : dst[k] + acc[k];
+      for (int k = 0; k < 8; ++k)
+        if (c0 + k < EW) {
+          d0[k] = first ? acc[k].x : d0[k] + acc[k].x;
+          d1[k] = first ? acc[k].y : d1[k] + acc[k].y;
+        }
     }
   }
 }
@@ -288,7 +313,7 @@ __device__ __forceinline__ Px bin_px(const FrameParams& p, float gx, float gy) {
   int db = (int)((atan2_nz(gy, gx) + kPi) * p.dir_scale);  // NaN for (0,0) -> 0
   db = db >= p.dir_bins ? db - p.dir_bins : db;
   db = max(db, 0);
-  o.lut = p.lut + ((long long)max(mb, 0) * p.dir_bins + db) * 4;
+  o.lut = p.lut + (max(mb, 0) * p.dir_bins + db) * 4;  // < 2^31 / 4 bins (host-checked)
   return o;
 }
 
@@ -360,18 +385,27 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
     const float m[4] = {mm.x, mm.y, mm.z, mm.w};
     const float n[4] = {nn.x, nn.y, nn.z, nn.w};
     const bool top = (y == 0), bot = (y == p.H - 1);
-    const float sy = (top || bot) ? p.inv_p : p.inv_2p;
     float gxs[4], gys[4];
+    if (!__any_sync(__activemask(), top || bot || xg == 0 || xg + 4 >= p.W)) {
+      // interior: central differences only
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int x = xg + k;
-      const bool lft = (x == 0), rgt = (x == x_last);
-      const float xr = rgt ? c[k + 1] : c[k + 2];
-      const float xl = lft ? c[k + 1] : c[k];
-      gxs[k] = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
-      const float yb = bot ? c[k + 1] : n[k];
-      const float yt = top ? c[k + 1] : m[k];
-      gys[k] = (yb - yt) * sy;
+      for (int k = 0; k < 4; ++k) {
+        gxs[k] = (c[k + 2] - c[k]) * p.inv_2p;
+        gys[k] = (n[k] - m[k]) * p.inv_2p;
+      }
+    } else {
+      const float sy = (top || bot) ? p.inv_p : p.inv_2p;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int x = xg + k;
+        const bool lft = (x == 0), rgt = (x == x_last);
+        const float xr = rgt ? c[k + 1] : c[k + 2];
+        const float xl = lft ? c[k + 1] : c[k];
+        gxs[k] = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
+        const float yb = bot ? c[k + 1] : n[k];
+        const float yt = top ? c[k + 1] : m[k];
+        gys[k] = (yb - yt) * sy;
+      }
     }
     uint32_t q[12];
 #pragma unroll
@@ -535,25 +569,39 @@ __device__ void finalize_load(const FrameParams& p, long long env, double cnt, d
   load_store(s_dbl, l);
 }
 
-__device__ __forceinline__ void shift_halo(const FrameParams& p, float* inb, int LW, int R) {
-  // rows [RB, RB + 2R) -> [0, 2R); each thread owns whole columns and walks
-  // them in increasing row order, so the overlapping copy is safe.
-  for (int c = threadIdx.x; c < LW; c += kThreads)
-    for (int k = 0; k < 2 * R; ++k) inb[k * p.in_pitch + c] = inb[(RB + k) * p.in_pitch + c];
+__device__ __forceinline__ void shift_halo(const FrameParams& p, float* inb, int LW, int R, bool vec,
+                                           int cg, int cro, int cstep) {
+  // rows [RB, RB + 2R) -> [0, 2R).  Phases of RB destination rows never read
+  // what they write; a barrier separates the phases.
+  for (int m = 0; m < 2 * R; m += RB) {
+    const int rows = min(RB, 2 * R - m);
+    if (vec) {
+      for (int rr = cro; cro < cstep && rr < rows; rr += cstep) {
+        float4* d = reinterpret_cast<float4*>(inb + (m + rr) * p.in_pitch) + cg;
+        *d = *(reinterpret_cast<const float4*>(inb + (m + rr + RB) * p.in_pitch) + cg);
+      }
+    } else {
+      for (int c = threadIdx.x; c < LW; c += kThreads)
+        for (int k = 0; k < rows; ++k) inb[(m + k) * p.in_pitch + c] = inb[(m + k + RB) * p.in_pitch + c];
+    }
+    if (m + RB < 2 * R) __syncthreads();
+  }
 }
 
 // Depth -> indentation in place for one float4 group of one row, folding the
-// contact partials (own pixels only) and the row non-zero flag.
-__device__ __forceinline__ void convert4(const FrameParams& p, const Geo& g, float* row, int gr, int cg,
-                                         const bool cown[4], const double cxc[4], const bool cvr[4],
-                                         unsigned char* rownz, Red& red) {
+// contact partials (own pixels only) and the row non-zero flag.  The thread's
+// columns are fixed, so Sum w*xc is kept as per-column fp32 sums (same row
+// order for mirrored columns -> bitwise-equal sums) and multiplied by xc in
+// fp64 once at the end; Sum w*yc per row in fp64.
+__device__ __forceinline__ void convert4(const FrameParams& p, float* row, int gr, int cg,
+                                         const bool cown[4], const bool cvr[4], unsigned char* rownz,
+                                         Red& red, float colsum[4]) {
   float4* e = reinterpret_cast<float4*>(row) + cg;
   float4 v4 = *e;
   float v[4] = {v4.x, v4.y, v4.z, v4.w};
   const bool rown = gr >= 0 && gr < p.H;
-  const double yc = (double)gr + 0.5 - (double)p.half_h;
   bool nz = false;
-  double rowsum = 0.0;
+  float rowsum = 0.f;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const bool own = rown && cown[q];
@@ -562,15 +610,17 @@ __device__ __forceinline__ void convert4(const FrameParams& p, const Geo& g, flo
     if (own) {
       red.mx = fmaxf(red.mx, v[q]);
       const bool in = v[q] > p.threshold;
-      const double m = in ? (double)v[q] : 0.0;
+      const float m = in ? v[q] : 0.f;
       red.cnt += in ? 1.f : 0.f;
       rowsum += m;
-      red.swx = fma(m, cxc[q], red.swx);
+      colsum[q] += m;
     }
     nz |= (v[q] != 0.f) && cvr[q];
   }
-  red.sw += rowsum;
-  red.swy = fma(rowsum, yc, red.swy);
+  if (rown) {
+    red.sw += (double)rowsum;
+    red.swy = fma((double)rowsum, (double)gr + 0.5 - (double)p.half_h, red.swy);
+  }
   *e = make_float4(v[0], v[1], v[2], v[3]);
   if (nz) rownz[gr + p.R] = 1;
 }
@@ -652,6 +702,7 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
   __syncthreads();
 
   Red red = red_zero();
+  float colsum[4] = {0.f, 0.f, 0.f, 0.f};
   unsigned phase = 0;
   issue_rows(-R, RB + R, 0);  // block 0 window
 
@@ -689,8 +740,8 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
       const int nrows = (b == 0) ? RB + 2 * R : RB;
       if (vec_conv) {
         // threads past the last full sweep (cro >= cstep) would duplicate rows
-        for (int rr = cro; cro < cstep && rr < nrows; rr += cstep) convert4(p, g, inb + (slot + rr) * p.in_pitch, ga + rr,
-                                                          cg, cown, cxc, cvr, rownz, red);
+        for (int rr = cro; cro < cstep && rr < nrows; rr += cstep)
+          convert4(p, inb + (slot + rr) * p.in_pitch, ga + rr, cg, cown, cvr, rownz, red, colsum);
       } else {
         for (int it = tid; it < nrows * LW; it += kThreads) {
           const int rr = it / LW;
@@ -736,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
         if (lastl && !last) {
           // this block's input rows are consumed: shift the halo, then start
           // the next block's copy (overlaps the H pass and the shading)
-          shift_halo(p, inb, LW, R);
+          shift_halo(p, inb, LW, R, vec_conv, cg, cro, cstep);
           fence_proxy_async();
         }
         if (RL > 0) vpad(p, g, RL, vb);
@@ -760,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
       // exact zero: the blurred rows are 0
       for (int it = tid; it < RB * p.b_pitch; it += kThreads) bb[2 * p.b_pitch + it] = 0.f;
       if (!last) {
-        shift_halo(p, inb, LW, R);
+        shift_halo(p, inb, LW, R, vec_conv, cg, cro, cstep);
         fence_proxy_async();
       }
       __syncthreads();
@@ -806,6 +857,8 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
 
   // ---- reduction + env epilogue -------------------------------------------------
   if (p.finalize == 0) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red.swx = fma((double)colsum[q], cxc[q], red.swx);
   block_reduce(red, s_red);
   if (p.strips == 1) {
     if (tid == 0) finalize_load(p, g.env, red.cnt, red.sw, red.swx, red.swy, red.mx, red.nf, s_dbl);
