@@ -77,3 +77,12 @@ if len(sys.argv) > 4:
                 ph[name][1] += s
     for name, (v, s) in ph.items():
         print(f"PHASE {name:12s} instr {100 * v / tot_i:5.1f}%  ({v * 32 / float(os.environ.get('PIXELS', 1)):.1f}/px)  stall {100 * s / tot_s:5.1f}%")
+
+if os.environ.get("LINES"):
+    a, b = map(int, os.environ["LINES"].split("-"))
+    srcf = os.environ.get("SRC", "paper_2411_04776_b200/csrc/tac_frame.cu")
+    src = open(srcf).read().splitlines()
+    px = float(os.environ.get("PIXELS", 1))
+    for line, (v, s) in sorted((k, t) for k, t in agg.items() if k and k[0] == os.path.basename(srcf)):
+        if a <= line[1] <= b and v:
+            print(f"L{line[1]:5d} {v * 32 / px:6.2f}/px stall {100 * s / tot_s:5.1f}%  {src[line[1] - 1].strip()[:90]}")
