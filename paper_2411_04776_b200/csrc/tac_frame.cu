@@ -80,6 +80,32 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- named barriers (warp-specialised fused kernel) -------------------------
+// id 0: whole CTA; 1: blur group; 2: shade group; 3..5: ring slot FULL[s];
+// 6..8: ring slot EMPTY[s].  Groups are 320 threads (10 warps) each.
+enum : int { kBarBlur = 1, kBarShade = 2, kBarFull = 3, kBarEmpty = 3 + kSlots };
+
+// ring row of global row r (r >= -1); slots are RB-row aligned
+__device__ __forceinline__ int ring_row(int r) { return (r + kRing) % kRing; }
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ bool bar_or(int id, int n, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred pi, po;\n setp.ne.u32 pi, %1, 0;\n bar.red.or.pred po, %2, %3, pi;\n"
+      " selp.u32 %0, 1, 0, po;\n}\n"
+      : "=r"(r)
+      : "r"((uint32_t)v), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void bsync() { bar_sync(kBarBlur, kThreads); }
+
 // ---- per-CTA geometry -------------------------------------------------------
 struct Geo {
   long long env;
@@ -192,7 +218,7 @@ __device__ __forceinline__ void vpad(const FrameParams& p, const Geo& g, int RL,
 template <int RL>
 __device__ __forceinline__ void hpass(const FrameParams& p, const Geo& g, int lvl,
                                       const float* __restrict__ vb, float* __restrict__ bb,
-                                      bool first) {
+                                      bool first, int r0) {
   float2 w[RL + 1];
 #pragma unroll
   for (int i = 0; i <= RL; ++i) w[i] = make_float2(p.wh[lvl][i], p.wh[lvl][i]);
@@ -217,8 +243,8 @@ __device__ __forceinline__ void hpass(const FrameParams& p, const Geo& g, int lv
         if (t >= -RL && t <= RL) acc[k] = ffma2(w[t < 0 ? -t : t], v, acc[k]);
       }
     }
-    float* d0 = bb + (2 + rp) * p.b_pitch + (g.bx0 + c0 - g.bbase);
-    float* d1 = d0 + 8 * p.b_pitch;
+    float* d0 = bb + ring_row(r0 + rp) * p.b_pitch + (g.bx0 + c0 - g.bbase);
+    float* d1 = bb + ring_row(r0 + rp + 8) * p.b_pitch + (g.bx0 + c0 - g.bbase);
     if (c0 + 8 <= EW) {
       float4* a4 = reinterpret_cast<float4*>(d0);
       float4* b4 = reinterpret_cast<float4*>(d1);
@@ -247,14 +273,14 @@ __device__ __forceinline__ void hpass(const FrameParams& p, const Geo& g, int lv
 
 // Identity level (k == 1): bb (+)= in / L, straight from the input buffer.
 __device__ __forceinline__ void ident_level(const FrameParams& p, const Geo& g, int lvl,
-                                            const float* inb, float* bb, bool first) {
+                                            const float* inb, float* bb, bool first, int r0) {
   const float w = p.wh[lvl][0];
   const int EW = g.bx1 - g.bx0;
   for (int it = threadIdx.x; it < EW * RB; it += kThreads) {
     const int r = it / EW;
     const int c = g.bx0 + (it - r * EW);
     const float v = w * inb[(p.R + r) * p.in_pitch + (c - g.lx0)];
-    float* d = bb + (2 + r) * p.b_pitch + (c - g.bbase);
+    float* d = bb + ring_row(r0 + r) * p.b_pitch + (c - g.bbase);
     *d = first ? v : *d + v;
   }
 }
@@ -338,17 +364,17 @@ __device__ __forceinline__ void shade_one(const FrameParams& p, float gx, float 
 // to y_lo).  Four consecutive pixels per thread: float4 reads of the blurred
 // ring (conflict-free), x-neighbours by warp shuffle, 16-B background loads,
 // LUT gathers issued two pixels at a time, 12-B staged stores.
-__device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, int r0, int y_lo,
-                                           int y_hi, const float* __restrict__ bb,
-                                           uint8_t* __restrict__ stage) {
+__device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, int y_lo, int y_hi,
+                                           const float* __restrict__ bb, uint8_t* __restrict__ stage,
+                                           int gtid) {
   const int OW = g.x1 - g.x0;
   const int ng = (OW + 3) >> 2;
   const int sw3 = OW * 3;
   const int rows = y_hi - y_lo;
   const int step = kThreads / ng;  // rows per sweep (>= 1: strips are <= 4 * kThreads wide)
-  const int gi = threadIdx.x % ng;
-  const int ro = threadIdx.x / ng;
-  const int lane = threadIdx.x & 31;
+  const int gi = gtid % ng;
+  const int ro = gtid / ng;
+  const int lane = gtid & 31;
   const int xg = g.x0 + 4 * gi;
   const bool full = xg + 4 <= g.x1;
   const bool vec_bg = ((p.W & 3) == 0) && full;
@@ -359,10 +385,13 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
     const int yy = y0 + ro;
     const bool act = (ro < step) && (yy < rows);
     const int y = y_lo + (act ? yy : 0);
-    const float* rc = bb + (y - r0 + 2) * p.b_pitch + (xg - g.bbase);
+    // blurred ring: global row r lives in ring row (r mod kRing)
+    const float* rc = bb + ring_row(y) * p.b_pitch + (xg - g.bbase);
+    const float* rm = bb + ring_row(y - 1) * p.b_pitch + (xg - g.bbase);
+    const float* rp = bb + ring_row(y + 1) * p.b_pitch + (xg - g.bbase);
     const float4 cc = *reinterpret_cast<const float4*>(rc);
-    const float4 mm = *reinterpret_cast<const float4*>(rc - p.b_pitch);
-    const float4 nn = *reinterpret_cast<const float4*>(rc + p.b_pitch);
+    const float4 mm = *reinterpret_cast<const float4*>(rm);
+    const float4 nn = *reinterpret_cast<const float4*>(rp);
     float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
     float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
     if (!act) continue;
@@ -441,8 +470,8 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
 
 // staged rows -> global, one warp per row, 16 B per lane when aligned.
 __device__ __forceinline__ void store_rows(uint8_t* out_rows, long long row_stride,
-                                           const uint8_t* stage, int rows, int nbytes) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+                                           const uint8_t* stage, int rows, int nbytes, int gtid) {
+  const int lane = gtid & 31, wid = gtid >> 5, nw = kThreads / 32;
   for (int rr = wid; rr < rows; rr += nw) {
     uint8_t* dst = out_rows + rr * row_stride;
     const uint8_t* src = stage + rr * nbytes;
@@ -461,8 +490,8 @@ __device__ __forceinline__ void store_rows(uint8_t* out_rows, long long row_stri
 
 // Copy quantised-background rows (blocks whose blur is exactly zero).
 __device__ __forceinline__ void bg_rows(const FrameParams& p, const Geo& g, uint8_t* out, int y_lo,
-                                        int y_hi) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+                                        int y_hi, int gtid) {
+  const int lane = gtid & 31, wid = gtid >> 5, nw = kThreads / 32;
   const int nbytes = (g.x1 - g.x0) * 3;
   for (int y = y_lo + wid; y < y_hi; y += nw) {
     const long long o = ((long long)y * p.W + g.x0) * 3;
@@ -497,7 +526,7 @@ __device__ __forceinline__ Red red_zero() {
 
 // Fixed shuffle tree + fixed warp order: deterministic.  Result in thread 0.
 __device__ __forceinline__ void block_reduce(Red& v, double* s_red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x / 32;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     v.cnt += __shfl_xor_sync(0xffffffffu, v.cnt, o);
@@ -584,7 +613,7 @@ __device__ __forceinline__ void shift_halo(const FrameParams& p, float* inb, int
       for (int c = threadIdx.x; c < LW; c += kThreads)
         for (int k = 0; k < rows; ++k) inb[(m + k) * p.in_pitch + c] = inb[(m + k + RB) * p.in_pitch + c];
     }
-    if (m + RB < 2 * R) __syncthreads();
+    if (m + RB < 2 * R) bsync();
   }
 }
 
@@ -648,32 +677,40 @@ __device__ __forceinline__ void convert1(const FrameParams& p, const Geo& g, flo
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// Fused mode is warp-specialised: threads [0, 320) are the blur group (TMA,
+// conversion, V/H passes), threads [320, 640) the shade group (shading and
+// RGB stores).  They hand row blocks over through a 2-slot blurred ring with
+// FULL/EMPTY named barriers, so the shade group's LUT-gather latency overlaps
+// the blur group's FFMA2 work.  Blur-only and contact modes run the blur group
+// alone (320 threads).
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constant__ FrameParams p) {
+__global__ void __launch_bounds__(MODE == kModeFused ? 2 * kThreads : kThreads,
+                                  MODE == kModeFused ? 1 : 2)
+    frame_kernel(const __grid_constant__ FrameParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Geo g = make_geo(p, MODE);
   const int R = MODE == kModeContact ? 0 : p.R;
   const long long HW = (long long)p.H * p.W;
   const int tid = threadIdx.x;
+  const bool blur_group = tid < kThreads;
 
   float* inb = reinterpret_cast<float*>(smem_raw);
   float* vb = inb + p.in_rows * p.in_pitch;
-  float* bb = vb + RB * p.v_pitch;
-  // RB + 2 rows + 1 spare row: the last image row reads its (unused) lower
-  // neighbour one row past the ring
-  double* s_red = reinterpret_cast<double*>(bb + (RB + 3) * p.b_pitch);  // 10 warps x 8
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_red + (kThreads / 32) * 8);
+  float* bb = vb + RB * p.v_pitch;                                       // kRing rows
+  uint8_t* stage = reinterpret_cast<uint8_t*>(bb + kRing * p.b_pitch);  // shade group
+  double* s_red = reinterpret_cast<double*>(stage + ((p.stage_bytes + 15) & ~15));  // 20 warps x 8
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_red + 2 * (kThreads / 32) * 8);
   unsigned char* rownz = reinterpret_cast<unsigned char*>(bar + 1);  // index: global row + R
   int* s_int = reinterpret_cast<int*>(rownz + ((p.H + 2 * p.R + RB + 15) & ~15));
   __shared__ double s_dbl[8];
   __shared__ int s_flag;
-  uint8_t* stage = reinterpret_cast<uint8_t*>(vb);
+  __shared__ int s_nz[kSlots];  // per ring slot: the shaded rows may be non-zero
 
   const float* src = p.in + g.env * HW;
   const int LW = g.lx1 - g.lx0;
   const unsigned row_bytes = (unsigned)LW * 4u;
 
-  // rows [ga, gb) (global, unclamped) -> buffer rows starting at `slot`
+  // rows [ga, gb) (global, unclamped) -> buffer rows starting at `slot` (blur group)
   auto issue_rows = [&](int ga, int gb, int slot) {
     if (p.use_tma) {
       if (tid == 0) {
@@ -698,167 +735,189 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = tid; i < p.H + 2 * p.R + RB; i += kThreads) rownz[i] = 0;
+  for (int i = tid; i < p.H + 2 * p.R + RB; i += blockDim.x) rownz[i] = 0;
   __syncthreads();
 
   Red red = red_zero();
   float colsum[4] = {0.f, 0.f, 0.f, 0.f};
-  unsigned phase = 0;
-  issue_rows(-R, RB + R, 0);  // block 0 window
 
-  uint8_t* out = (MODE == kModeFused) ? p.rgb + g.env * HW * 3 : nullptr;
-
-  // conversion mapping: thread -> fixed float4 column group, rows strided
-  const int ng4 = LW >> 2;
-  const bool vec_conv = ((LW & 3) == 0) && ng4 > 0 && ng4 <= kThreads;
-  const int cg = vec_conv ? tid % ng4 : 0;
-  const int cro = vec_conv ? tid / ng4 : 0;
-  const int cstep = vec_conv ? kThreads / ng4 : 1;
-  bool cown[4], cvr[4];
-  double cxc[4];
+  if (blur_group) {
+    // ======================= blur group ========================================
+    unsigned phase = 0;
+    issue_rows(-R, RB + R, 0);  // block 0 window
+    // conversion mapping: thread -> fixed float4 column group, rows strided
+    const int ng4 = LW >> 2;
+    const bool vec_conv = ((LW & 3) == 0) && ng4 > 0 && ng4 <= kThreads;
+    const int cg = vec_conv ? tid % ng4 : 0;
+    const int cro = vec_conv ? tid / ng4 : 0;
+    const int cstep = vec_conv ? kThreads / ng4 : 1;
+    bool cown[4], cvr[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int gx = g.lx0 + 4 * cg + q;
-    cown[q] = gx >= g.x0 && gx < g.x1;
-    cvr[q] = gx >= g.vx0 && gx < g.vx1;
-    cxc[q] = (double)gx + 0.5 - (double)p.half_w;
-  }
-
-  for (int b = 0; b < g.nblocks; ++b) {
-    const int r0 = b * RB;
-    const bool last = (b == g.nblocks - 1);
-    // ---- wait for this block's rows, convert the new ones -------------------
-    if (p.use_tma) {
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-    } else {
-      __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+      const int gx = g.lx0 + 4 * cg + q;
+      cown[q] = gx >= g.x0 && gx < g.x1;
+      cvr[q] = gx >= g.vx0 && gx < g.vx1;
     }
-    {
-      const int ga = (b == 0) ? r0 - R : r0 + R;  // first new global row
-      const int slot = (b == 0) ? 0 : 2 * R;
-      const int nrows = (b == 0) ? RB + 2 * R : RB;
-      if (vec_conv) {
-        // threads past the last full sweep (cro >= cstep) would duplicate rows
-        for (int rr = cro; cro < cstep && rr < nrows; rr += cstep)
-          convert4(p, inb + (slot + rr) * p.in_pitch, ga + rr, cg, cown, cvr, rownz, red, colsum);
+
+    for (int b = 0; b < g.nblocks; ++b) {
+      const int r0 = b * RB;
+      const bool last = (b == g.nblocks - 1);
+      // ---- wait for this block's rows, convert the new ones -----------------
+      if (p.use_tma) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
       } else {
-        for (int it = tid; it < nrows * LW; it += kThreads) {
-          const int rr = it / LW;
-          const int cc = it - rr * LW;
-          convert1(p, g, inb + (slot + rr) * p.in_pitch + cc, ga + rr, g.lx0 + cc, rownz, red);
+        bsync();
+      }
+      {
+        const int ga = (b == 0) ? r0 - R : r0 + R;  // first new global row
+        const int slot = (b == 0) ? 0 : 2 * R;
+        const int nrows = (b == 0) ? RB + 2 * R : RB;
+        if (vec_conv) {
+          // threads past the last full sweep (cro >= cstep) would duplicate rows
+          for (int rr = cro; cro < cstep && rr < nrows; rr += cstep)
+            convert4(p, inb + (slot + rr) * p.in_pitch, ga + rr, cg, cown, cvr, rownz, red, colsum);
+        } else {
+          for (int it = tid; it < nrows * LW; it += kThreads) {
+            const int rr = it / LW;
+            const int cc = it - rr * LW;
+            convert1(p, g, inb + (slot + rr) * p.in_pitch + cc, ga + rr, g.lx0 + cc, rownz, red);
+          }
         }
       }
-    }
-    __syncthreads();
+      bsync();
 
-    if (MODE == kModeContact) {
-      if (!last) {
-        fence_proxy_async();
-        __syncthreads();
-        issue_rows(r0 + RB, r0 + 2 * RB, 0);
+      if (MODE == kModeContact) {
+        if (!last) {
+          fence_proxy_async();
+          bsync();
+          issue_rows(r0 + RB, r0 + 2 * RB, 0);
+        }
+        continue;
       }
-      continue;
-    }
 
-    // ---- blur ------------------------------------------------------------------
-    int any = 0;
-    for (int i = tid; i < RB + 2 * R; i += kThreads) any |= rownz[r0 + i];  // rows r0-R .. r0+RB+R-1
-    any = __syncthreads_or(any);
-    if (any) {
-      for (int l = 0; l < p.n_levels; ++l) {
-        const int RL = p.radius[l];
-        const bool lastl = (l == p.n_levels - 1);
-        if (RL == 0) {
-          ident_level(p, g, l, inb, bb, l == 0);
-        } else {
-          switch (RL) {
+      // ---- blur into ring slot b & 1 --------------------------------------------
+      bool any = false;
+      for (int i = tid; i < RB + 2 * R; i += kThreads) any |= rownz[r0 + i] != 0;  // rows r0-R..r0+RB+R-1
+      any = bar_or(kBarBlur, kThreads, any);
+      // slot b % kSlots still holds block b-kSlots, whose last rows the shade
+      // group reads until it has finished block b-kSlots+1
+      if (MODE == kModeFused && b >= kSlots) bar_sync(kBarEmpty + b % kSlots, 2 * kThreads);
+      if (any) {
+        for (int l = 0; l < p.n_levels; ++l) {
+          const int RL = p.radius[l];
+          const bool lastl = (l == p.n_levels - 1);
+          if (RL == 0) {
+            ident_level(p, g, l, inb, bb, l == 0, r0);
+          } else {
+            switch (RL) {
 #define X(r)                    \
   case r:                       \
     vpass<r>(p, g, l, inb, vb); \
     break;
-            TAC_RADIUS_CASES(X)
+              TAC_RADIUS_CASES(X)
 #undef X
-            default:
-              break;
+              default:
+                break;
+            }
           }
+          bsync();
+          if (lastl && !last) {
+            // this block's input rows are consumed: shift the halo, then start
+            // the next block's copy (overlaps the H pass)
+            shift_halo(p, inb, LW, R, vec_conv, cg, cro, cstep);
+            fence_proxy_async();
+          }
+          if (RL > 0) vpad(p, g, RL, vb);
+          bsync();
+          if (lastl && !last) issue_rows(r0 + RB + R, r0 + 2 * RB + R, 2 * R);
+          if (RL > 0) {
+            switch (RL) {
+#define X(r)                                   \
+  case r:                                      \
+    hpass<r>(p, g, l, vb, bb, l == 0, r0);     \
+    break;
+              TAC_RADIUS_CASES(X)
+#undef X
+              default:
+                break;
+            }
+          }
+          bsync();
         }
-        __syncthreads();
-        if (lastl && !last) {
-          // this block's input rows are consumed: shift the halo, then start
-          // the next block's copy (overlaps the H pass and the shading)
+      } else {
+        // exact zero: the blurred rows are 0
+        for (int it = tid; it < RB * p.b_pitch; it += kThreads)
+          bb[ring_row(r0) * p.b_pitch + it] = 0.f;
+        if (!last) {
           shift_halo(p, inb, LW, R, vec_conv, cg, cro, cstep);
           fence_proxy_async();
         }
-        if (RL > 0) vpad(p, g, RL, vb);
-        __syncthreads();
-        if (lastl && !last) issue_rows(r0 + RB + R, r0 + 2 * RB + R, 2 * R);
-        if (RL > 0) {
-          switch (RL) {
-#define X(r)                            \
-  case r:                               \
-    hpass<r>(p, g, l, vb, bb, l == 0);  \
-    break;
-            TAC_RADIUS_CASES(X)
-#undef X
-            default:
-              break;
-          }
-        }
-        __syncthreads();
+        bsync();
+        if (!last) issue_rows(r0 + RB + R, r0 + 2 * RB + R, 2 * R);
       }
-    } else {
-      // exact zero: the blurred rows are 0
-      for (int it = tid; it < RB * p.b_pitch; it += kThreads) bb[2 * p.b_pitch + it] = 0.f;
-      if (!last) {
-        shift_halo(p, inb, LW, R, vec_conv, cg, cro, cstep);
-        fence_proxy_async();
-      }
-      __syncthreads();
-      if (!last) issue_rows(r0 + RB + R, r0 + 2 * RB + R, 2 * R);
-    }
 
-    // ---- outputs ---------------------------------------------------------------
-    if (p.blurred != nullptr) {
-      float* dst = p.blurred + g.env * HW;
-      const int OW = g.x1 - g.x0;
-      const int nr = min(RB, p.H - r0);
-      for (int it = tid; it < nr * OW; it += kThreads) {
-        const int rr = it / OW;
-        const int x = g.x0 + (it - rr * OW);
-        dst[(long long)(r0 + rr) * p.W + x] = bb[(2 + rr) * p.b_pitch + (x - g.bbase)];
+      // ---- outputs ----------------------------------------------------------------
+      if (p.blurred != nullptr) {
+        float* dst = p.blurred + g.env * HW;
+        const int OW = g.x1 - g.x0;
+        const int nr = min(RB, p.H - r0);
+        for (int it = tid; it < nr * OW; it += kThreads) {
+          const int rr = it / OW;
+          const int x = g.x0 + (it - rr * OW);
+          dst[(long long)(r0 + rr) * p.W + x] = bb[ring_row(r0 + rr) * p.b_pitch + (x - g.bbase)];
+        }
+      }
+      if (MODE == kModeFused) {
+        // may the rows the shade group shades for this block be non-zero?
+        // (rows y-1..y+1 of y in [y_lo, y_hi) read input rows [y_lo-1-R, y_hi+R])
+        if (tid == 0) {
+          const int y_lo = max(r0 - 1, 0);
+          const int y_hi = last ? p.H : r0 + RB - 1;
+          int nz = 0;
+          for (int gr = max(y_lo - 1 - p.R, -p.R); gr <= min(y_hi + p.R, p.H + p.R - 1); ++gr)
+            nz |= rownz[gr + p.R];
+          s_nz[b % kSlots] = nz;
+        }
+        bar_arrive(kBarFull + b % kSlots, 2 * kThreads);
+      } else {
+        bsync();
       }
     }
-    if (MODE == kModeFused) {
+  } else if (MODE == kModeFused) {
+    // ======================= shade group =======================================
+    const int gtid = tid - kThreads;
+    uint8_t* out = p.rgb + g.env * HW * 3;
+    for (int b = 0; b < g.nblocks; ++b) {
+      const int r0 = b * RB;
+      const bool last = (b == g.nblocks - 1);
+      bar_sync(kBarFull + b % kSlots, 2 * kThreads);
       const int y_lo = max(r0 - 1, 0);
       const int y_hi = last ? p.H : r0 + RB - 1;
-      // blurred rows y-1..y+1 of every shaded row are exactly zero iff input
-      // rows [y_lo-1-R, y_hi+R] are zero
-      int nz = 0;
-      for (int i = tid; i < (y_hi - y_lo) + 2 + 2 * p.R; i += kThreads) {
-        const int gr = y_lo - 1 - p.R + i;
-        if (gr >= -p.R && gr < p.H + p.R) nz |= rownz[gr + p.R];
-      }
-      nz = __syncthreads_or(nz);
-      if (nz) {
-        shade_rows(p, g, r0, y_lo, y_hi, bb, stage);
-        __syncthreads();
+      if (s_nz[b % kSlots]) {
+        shade_rows(p, g, y_lo, y_hi, bb, stage, gtid);
+        bar_sync(kBarShade, kThreads);
         store_rows(out + ((long long)y_lo * p.W + g.x0) * 3, (long long)p.W * 3, stage, y_hi - y_lo,
-                   (g.x1 - g.x0) * 3);
+                   (g.x1 - g.x0) * 3, gtid);
+        bar_sync(kBarShade, kThreads);  // stage is reused by the next block
       } else {
-        bg_rows(p, g, out, y_lo, y_hi);
+        bg_rows(p, g, out, y_lo, y_hi, gtid);
       }
-      __syncthreads();
-      // keep blurred rows r0+RB-2, r0+RB-1 for the next block's gradient
-      for (int it = tid; it < 2 * p.b_pitch; it += kThreads) bb[it] = bb[RB * p.b_pitch + it];
+      // block b-1's slot (= block b+kSlots-1's) is no longer read
+      if (b >= 1 && b + kSlots - 1 < g.nblocks) bar_arrive(kBarEmpty + (b + kSlots - 1) % kSlots, 2 * kThreads);
     }
-    __syncthreads();
   }
 
   // ---- reduction + env epilogue -------------------------------------------------
   if (p.finalize == 0) return;
+  if (blur_group) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) red.swx = fma((double)colsum[q], cxc[q], red.swx);
+    for (int q = 0; q < 4; ++q) {
+      const int cgq = ((LW & 3) == 0 && (LW >> 2) > 0 && (LW >> 2) <= kThreads) ? tid % (LW >> 2) : 0;
+      red.swx = fma((double)colsum[q], (double)(g.lx0 + 4 * cgq + q) + 0.5 - (double)p.half_w, red.swx);
+    }
+  }
+  __syncthreads();  // all RGB rows written, s_red free
   block_reduce(red, s_red);
   if (p.strips == 1) {
     if (tid == 0) finalize_load(p, g.env, red.cnt, red.sw, red.swx, red.swy, red.mx, red.nf, s_dbl);
@@ -908,8 +967,9 @@ __global__ void __launch_bounds__(kThreads, 2) frame_kernel(const __grid_constan
 
 size_t frame_smem_bytes(const FrameParams& p) {
   size_t bytes = sizeof(float) * ((size_t)p.in_rows * p.in_pitch + (size_t)RB * p.v_pitch +
-                                  (size_t)(RB + 3) * p.b_pitch) +
-                 sizeof(double) * (kThreads / 32) * 8;
+                                  (size_t)kRing * p.b_pitch);
+  bytes += (p.stage_bytes + 15) & ~15;
+  bytes += sizeof(double) * 2 * (kThreads / 32) * 8;
   bytes += sizeof(uint64_t);
   bytes += (p.H + 2 * p.R + RB + 15) & ~15;
   bytes += 2 * sizeof(int) * (size_t)p.mg.rows * p.mg.cols;
@@ -924,7 +984,7 @@ static cudaError_t launch_mode(const FrameParams& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const long long blocks = p.n_env * (long long)p.strips;
   if (blocks == 0) return cudaSuccess;
-  frame_kernel<MODE><<<(unsigned)blocks, kThreads, smem, s>>>(p);
+  frame_kernel<MODE><<<(unsigned)blocks, MODE == kModeFused ? 2 * kThreads : kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,9 @@ namespace tac {
 // Strip-streaming frame kernel geometry (see tac_frame.cu).
 constexpr int RB = 16;        // rows per row block (vertical-pass register block)
 constexpr int KH = 16;        // horizontal-pass outputs per thread
-constexpr int kThreads = 320; // threads per CTA (= 320 columns of a 320-wide strip)
+constexpr int kThreads = 320; // threads per group (= 320 columns of a 320-wide strip)
+constexpr int kSlots = 3;      // blurred ring slots: blur runs up to two row blocks ahead of shading
+constexpr int kRing = kSlots * RB;
 constexpr int kSumFields = 8; // per-strip partial / per-env summary width
 
 // Frame-kernel modes.
@@ -41,8 +43,8 @@ struct FrameParams {
   int R;                 // max radius over levels (vertical halo rows)
   int in_rows, in_pitch; // input buffer: in_rows x in_pitch floats
   int v_pitch;           // vertical-pass buffer: RB x v_pitch floats (odd pitch)
-  int b_pitch;           // blurred ring: (RB + 2 (+1 spare)) x b_pitch floats (multiple of 4)
-  int stage_bytes;       // uint8 RGB staging (aliases the vertical-pass buffer)
+  int b_pitch;           // blurred ring: kRing x b_pitch floats (multiple of 4, 4 x odd)
+  int stage_bytes;       // uint8 RGB staging of the shade group
   int use_tma;           // rows 16-B aligned -> cp.async.bulk row loads
   // pyramid
   int n_levels;
