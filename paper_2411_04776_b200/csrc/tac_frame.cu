@@ -371,7 +371,7 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
   const int ng = (OW + 3) >> 2;
   const int sw3 = OW * 3;
   const int rows = y_hi - y_lo;
-  const int step = kThreads / ng;  // rows per sweep (>= 1: strips are <= 4 * kThreads wide)
+  const int step = kShadeThreads / ng;  // rows per sweep (>= 1: strips are <= 4 * kShadeThreads wide)
   const int gi = gtid % ng;
   const int ro = gtid / ng;
   const int lane = gtid & 31;
@@ -471,7 +471,7 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
 // staged rows -> global, one warp per row, 16 B per lane when aligned.
 __device__ __forceinline__ void store_rows(uint8_t* out_rows, long long row_stride,
                                            const uint8_t* stage, int rows, int nbytes, int gtid) {
-  const int lane = gtid & 31, wid = gtid >> 5, nw = kThreads / 32;
+  const int lane = gtid & 31, wid = gtid >> 5, nw = kShadeThreads / 32;
   for (int rr = wid; rr < rows; rr += nw) {
     uint8_t* dst = out_rows + rr * row_stride;
     const uint8_t* src = stage + rr * nbytes;
@@ -491,7 +491,7 @@ __device__ __forceinline__ void store_rows(uint8_t* out_rows, long long row_stri
 // Copy quantised-background rows (blocks whose blur is exactly zero).
 __device__ __forceinline__ void bg_rows(const FrameParams& p, const Geo& g, uint8_t* out, int y_lo,
                                         int y_hi, int gtid) {
-  const int lane = gtid & 31, wid = gtid >> 5, nw = kThreads / 32;
+  const int lane = gtid & 31, wid = gtid >> 5, nw = kShadeThreads / 32;
   const int nbytes = (g.x1 - g.x0) * 3;
   for (int y = y_lo + wid; y < y_hi; y += nw) {
     const long long o = ((long long)y * p.W + g.x0) * 3;
@@ -684,7 +684,7 @@ __device__ __forceinline__ void convert1(const FrameParams& p, const Geo& g, flo
 // the blur group's FFMA2 work.  Blur-only and contact modes run the blur group
 // alone (320 threads).
 template <int MODE>
-__global__ void __launch_bounds__(MODE == kModeFused ? 2 * kThreads : kThreads,
+__global__ void __launch_bounds__(MODE == kModeFused ? kThreads + kShadeThreads : kThreads,
                                   MODE == kModeFused ? 1 : 2)
     frame_kernel(const __grid_constant__ FrameParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? 2 * kThreads : kThreads,
   float* vb = inb + p.in_rows * p.in_pitch;
   float* bb = vb + RB * p.v_pitch;                                       // kRing rows
   uint8_t* stage = reinterpret_cast<uint8_t*>(bb + kRing * p.b_pitch);  // shade group
-  double* s_red = reinterpret_cast<double*>(stage + ((p.stage_bytes + 15) & ~15));  // 20 warps x 8
+  double* s_red = reinterpret_cast<double*>(stage + ((p.stage_bytes + 15) & ~15));  // <= 20 warps x 8
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_red + 2 * (kThreads / 32) * 8);
   unsigned char* rownz = reinterpret_cast<unsigned char*>(bar + 1);  // index: global row + R
   int* s_int = reinterpret_cast<int*>(rownz + ((p.H + 2 * p.R + RB + 15) & ~15));
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? 2 * kThreads : kThreads,
       any = bar_or(kBarBlur, kThreads, any);
       // slot b % kSlots still holds block b-kSlots, whose last rows the shade
       // group reads until it has finished block b-kSlots+1
-      if (MODE == kModeFused && b >= kSlots) bar_sync(kBarEmpty + b % kSlots, 2 * kThreads);
+      if (MODE == kModeFused && b >= kSlots) bar_sync(kBarEmpty + b % kSlots, kThreads + kShadeThreads);
       if (any) {
         for (int l = 0; l < p.n_levels; ++l) {
           const int RL = p.radius[l];
@@ -879,7 +879,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? 2 * kThreads : kThreads,
             nz |= rownz[gr + p.R];
           s_nz[b % kSlots] = nz;
         }
-        bar_arrive(kBarFull + b % kSlots, 2 * kThreads);
+        bar_arrive(kBarFull + b % kSlots, kThreads + kShadeThreads);
       } else {
         bsync();
       }
@@ -891,20 +891,20 @@ __global__ void __launch_bounds__(MODE == kModeFused ? 2 * kThreads : kThreads,
     for (int b = 0; b < g.nblocks; ++b) {
       const int r0 = b * RB;
       const bool last = (b == g.nblocks - 1);
-      bar_sync(kBarFull + b % kSlots, 2 * kThreads);
+      bar_sync(kBarFull + b % kSlots, kThreads + kShadeThreads);
       const int y_lo = max(r0 - 1, 0);
       const int y_hi = last ? p.H : r0 + RB - 1;
       if (s_nz[b % kSlots]) {
         shade_rows(p, g, y_lo, y_hi, bb, stage, gtid);
-        bar_sync(kBarShade, kThreads);
+        bar_sync(kBarShade, kShadeThreads);
         store_rows(out + ((long long)y_lo * p.W + g.x0) * 3, (long long)p.W * 3, stage, y_hi - y_lo,
                    (g.x1 - g.x0) * 3, gtid);
-        bar_sync(kBarShade, kThreads);  // stage is reused by the next block
+        bar_sync(kBarShade, kShadeThreads);  // stage is reused by the next block
       } else {
         bg_rows(p, g, out, y_lo, y_hi, gtid);
       }
       // block b-1's slot (= block b+kSlots-1's) is no longer read
-      if (b >= 1 && b + kSlots - 1 < g.nblocks) bar_arrive(kBarEmpty + (b + kSlots - 1) % kSlots, 2 * kThreads);
+      if (b >= 1 && b + kSlots - 1 < g.nblocks) bar_arrive(kBarEmpty + (b + kSlots - 1) % kSlots, kThreads + kShadeThreads);
     }
   }
 
@@ -984,7 +984,7 @@ static cudaError_t launch_mode(const FrameParams& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const long long blocks = p.n_env * (long long)p.strips;
   if (blocks == 0) return cudaSuccess;
-  frame_kernel<MODE><<<(unsigned)blocks, MODE == kModeFused ? 2 * kThreads : kThreads, smem, s>>>(p);
+  frame_kernel<MODE><<<(unsigned)blocks, MODE == kModeFused ? kThreads + kShadeThreads : kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 

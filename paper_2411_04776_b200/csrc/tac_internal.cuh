@@ -12,6 +12,10 @@ namespace tac {
 constexpr int RB = 16;        // rows per row block (vertical-pass register block)
 constexpr int KH = 16;        // horizontal-pass outputs per thread
 constexpr int kThreads = 320; // threads per group (= 320 columns of a 320-wide strip)
+#ifndef TAC_SHADE_WARPS
+#define TAC_SHADE_WARPS 10
+#endif
+constexpr int kShadeThreads = 32 * TAC_SHADE_WARPS;  // shade group of the fused kernel
 constexpr int kSlots = 3;      // blurred ring slots: blur runs up to two row blocks ahead of shading
 constexpr int kRing = kSlots * RB;
 constexpr int kSumFields = 8; // per-strip partial / per-env summary width
