@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[i] (1, 2 or 3)")
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0, help="cpu_baseline sample (wall s)")
+    ap.add_argument("--ref-seconds", type=float, default=90.0, help="--impl reference total budget (wall s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
@@ -50,10 +51,12 @@ def parse():
 
 
 # --------------------------------------------------------------------------- CPU arm
-def _cpu_worker(args):
-    """Time the oracle port on a slice of frames (one single-threaded process)."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    cfg_index, seed, start, count = args
+_W = {}
+
+
+def _cpu_init(cfg_index, seed, worker_frames):
+    """Pool initializer: one single-threaded process holding a few distinct frames."""
+    os.environ["OMP_NUM_THREADS"] = "1"
     import torch
 
     torch.set_num_threads(1)
@@ -62,30 +65,45 @@ def _cpu_worker(args):
 
     cfg, _ = synthetic.baseline_config(cfg_index, seed)
     h, w = cfg.sensor.image_size
-    p = synthetic.indenters(start + count, h, w, seed + 10)
-    sel = synthetic.IndenterParams(*(getattr(p, f)[start:] for f in
-                                     ("kind", "pen", "cx", "cy", "yaw", "perm", "off")))
-    depth = synthetic.height_maps(sel, h, w, dtype=torch.float64).numpy()
-    shear, twist = synthetic.loads(start + count, seed + 20)
-    orc = FastOracle(cfg)
-    orc.run(depth[0], shear[start], twist[start])  # warm
+    rank = os.getpid() % 1000
+    p = synthetic.indenters(worker_frames, h, w, seed + 10 + rank)
+    _W["depth"] = synthetic.height_maps(p, h, w, dtype=torch.float64).numpy()
+    _W["shear"], _W["twist"] = synthetic.loads(worker_frames, seed + 20 + rank)
+    _W["orc"] = FastOracle(cfg)
+    _W["orc"].run(_W["depth"][0], _W["shear"][0], _W["twist"][0])  # warm
+
+
+def _cpu_job(count):
+    """Run `count` frames of the oracle port; returns (frames, seconds)."""
+    d, sh, tw, orc = _W["depth"], _W["shear"], _W["twist"], _W["orc"]
     t0 = time.perf_counter()
     for i in range(count):
-        orc.run(depth[i], shear[start + i], twist[start + i])
+        k = i % len(d)
+        orc.run(d[k], sh[k], tw[k])
     return count, time.perf_counter() - t0
 
 
-def cpu_rate(cfg_index, seed, cores, frames_per_core):
-    """Aggregate frames/s of the oracle port on `cores` processes."""
-    jobs = [(cfg_index, seed, i * frames_per_core, frames_per_core) for i in range(cores)]
-    ctx = mproc.get_context("spawn")
-    t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_cpu_worker, jobs)
-    wall = time.perf_counter() - t0
-    frames = sum(r[0] for r in res)
-    per_core = statistics.mean(r[0] / r[1] for r in res)
-    return frames, per_core * cores, per_core, wall
+class CpuArm:
+    """A process pool (one single-threaded worker per host core) timing the
+    oracle port of the reference CPU path on configs[i] frames."""
+
+    def __init__(self, cfg_index, seed, cores, worker_frames=8):
+        self.cores = cores
+        ctx = mproc.get_context("spawn")
+        self.pool = ctx.Pool(cores, initializer=_cpu_init, initargs=(cfg_index, seed, worker_frames))
+        self.per_frame = max(r[1] / r[0] for r in self.pool.map(_cpu_job, [2] * cores))
+
+    def step(self, frames_per_core):
+        """Aggregate frames/s over all cores for one bounded sample."""
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_job, [frames_per_core] * self.cores)
+        wall = time.perf_counter() - t0
+        frames = sum(r[0] for r in res)
+        return frames / wall, statistics.mean(r[0] / r[1] for r in res), wall, frames
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def host_cores():
@@ -93,13 +111,6 @@ def host_cores():
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
-
-
-def calibrate_frames_per_core(cfg_index, seed, seconds):
-    """Frames per core so the pool spends ~`seconds` of wall time."""
-    n, dt = _cpu_worker((cfg_index, seed, 0, 2))
-    per = dt / n
-    return max(2, int(seconds / per))
 
 
 # --------------------------------------------------------------------------- helpers
@@ -167,20 +178,13 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def fma_per_frame(cfg, tx, ty):
-    """FFMA count per frame of the blur as planned (V pass on the halo-extended
-    columns, H pass on the ring-extended tile), ignoring zero-tile skips."""
+def fma_per_frame(cfg):
+    """Dense FFMA count per frame of the strip-streaming blur: per level a
+    vertical and a horizontal pass of (2r+1) taps over every pixel of the
+    16-row blocks (zero-block skips not counted)."""
     h, w = cfg.sensor.image_size
-    total = 0
-    for y0 in range(0, h, ty):
-        for x0 in range(0, w, tx):
-            x1, y1 = min(x0 + tx, w), min(y0 + ty, h)
-            ex0, ex1, ey0, ey1 = max(x0 - 1, 0), min(x1 + 1, w), max(y0 - 1, 0), min(y1 + 1, h)
-            EW, EH = ex1 - ex0, ey1 - ey0
-            for _, r in cfg.levels:
-                if r:
-                    total += EH * (EW + 2 * r) * (2 * r + 1) + EH * EW * (2 * r + 1)
-    return total
+    rows = -(-h // 16) * 16
+    return sum(2 * (2 * r + 1) * rows * w for _, r in cfg.levels if r)
 
 
 def algorithmic_bytes(cfg):
@@ -191,18 +195,22 @@ def algorithmic_bytes(cfg):
 
 # --------------------------------------------------------------------------- arms
 def run_reference(a, rank, world):
-    """--impl reference: the oracle port of the reference CPU path on all host cores."""
+    """--impl reference: the oracle port of the reference CPU path on all host
+    cores, each step a bounded sample so the whole run stays within minutes."""
     if rank != 0:
         return
     cores = host_cores()
-    fpc = calibrate_frames_per_core(a.config, a.seed, 0.75)
+    arm = CpuArm(a.config, a.seed, cores)
+    budget = max(0.5, a.ref_seconds / max(1, a.steps + a.warmup))  # wall seconds per step
+    fpc = max(1, int(budget / arm.per_frame))
     for _ in range(a.warmup):
-        cpu_rate(a.config, a.seed, cores, max(1, fpc // 4))
+        arm.step(fpc)
     vals, walls = [], []
     for _ in range(a.steps):
-        frames, agg, per_core, wall = cpu_rate(a.config, a.seed, cores, fpc)
-        vals.append(agg)
+        v, _, wall, _ = arm.step(fpc)
+        vals.append(v)
         walls.append(wall)
+    arm.close()
     v = statistics.median(vals)
     from paper_2411_04776_b200 import synthetic
 
@@ -221,7 +229,7 @@ def run_reference(a, rank, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"configs[{a.config}] sample", "envs_per_step": cores * fpc,
+        "config": {"workload": f"configs[{a.config}] sample", "frames_per_step": cores * fpc,
                    "H": cfg.sensor.image_size[0], "W": cfg.sensor.image_size[1],
                    "sigmas": [s for s, _ in cfg.levels], "markers": list(cfg.sensor.marker_grid),
                    "parallelism": f"cpu x{cores} processes"},
@@ -341,7 +349,7 @@ def run_ours(a, rank, world, local_rank):
     achieved = per_launch / (k_ms / 1e3) / 1e9
     props = torch.cuda.get_device_properties(dev)
     clocks = clk.result()
-    fma = fma_per_frame(cfg, int(os.environ.get("TAC_TILE_X", 64)), int(os.environ.get("TAC_TILE_Y", 30)))
+    fma = fma_per_frame(cfg)
     sm_ghz = (clocks["sm_mhz"] or 1965) / 1e3
     fma_peak = props.multi_processor_count * 128 * sm_ghz * 1e9
     traffic = None
@@ -400,13 +408,15 @@ def run_ours(a, rank, world, local_rank):
         line["e2e"] = e2e
     if world == 1 and not a.no_cpu_baseline:
         cores = host_cores()
-        fpc = calibrate_frames_per_core(a.config, a.seed, a.cpu_seconds)
-        frames, agg, per_core, wall = cpu_rate(a.config, a.seed, cores, fpc)
+        arm = CpuArm(a.config, a.seed, cores)
+        fpc = max(2, int(a.cpu_seconds / arm.per_frame))
+        agg, per_core, wall, frames = arm.step(fpc)
+        arm.close()
         line["cpu_baseline"] = {
             "value": agg, "unit": UNIT, "cores": cores, "kind": "port",
             "per_core": per_core,
-            "sample": f"{frames} frames ({cores}x{fpc}) of configs[{a.config}], oracle port, f64, "
-                      f"{wall:.1f} s wall",
+            "sample": f"{frames} frames ({cores}x{fpc}) of configs[{a.config}], oracle port "
+                      f"(REF/tactile.py:219 scipy blur + numpy gradient/LUT/markers), f64, {wall:.1f} s wall",
         }
     print(json.dumps(line), flush=True)
 
