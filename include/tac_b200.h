@@ -40,6 +40,8 @@ extern "C" {
 
 #define TAC_MAX_LEVELS 8
 #define TAC_MAX_RADIUS 24
+#define TAC_MAX_LIGHTS 4
+#define TAC_MAX_SHADOW_STEPS 256
 
 enum {
   TAC_OK = 0,
@@ -87,6 +89,14 @@ typedef struct tac_config {
   double contact_threshold;          /* > 0 */
   int32_t dot_radius;                /* 0..12 */
   uint8_t dot_color[3];
+
+  /* add_shadows (REF/optical.py:261-300).  shadow_factor == 1.0 disables the
+   * stage (the reference's exact identity, REF/optical.py:281-282). */
+  int32_t n_lights;                          /* 0..TAC_MAX_LIGHTS */
+  double light_dir[TAC_MAX_LIGHTS][3];       /* surface -> light, any length */
+  double shadow_factor;                      /* in [0, 1] */
+  int32_t shadow_steps;                      /* max_steps, 1..TAC_MAX_SHADOW_STEPS */
+  double shadow_softness;                    /* soft-edge width, m, > 0 */
 } tac_config;
 
 typedef struct tac_ctx tac_ctx;
@@ -153,6 +163,15 @@ int tac_marker_displacements(const tac_ctx* ctx, const double* loads, float* dis
 int tac_render_markers(const tac_ctx* ctx, const float* disp, uint8_t* rgb,
                        int64_t n_env, void* stream);
 
+/* add_shadows (REF/optical.py:261-300): per light, march max_steps pixels
+ * toward the light over the elevation (-depth, or the indentation for
+ * TAC_INPUT_INDENTATION), occ = max_s(elev(p + o_s) - elev(p) - s * rise),
+ * weight = clip(occ / softness, 0, 1), factor *= 1 - (1 - shadow_factor) * weight.
+ * in: [N,H,W]; factor (nullable): [N,H,W] fp32 product over lights;
+ * rgb (nullable): [N,H,W,3] fp32 multiplied in place. */
+int tac_shadow(const tac_ctx* ctx, const float* in, int32_t input_kind, float* factor,
+               float* rgb, int64_t n_env, void* stream);
+
 /* The fused path: one launch per call.  depth -> rgb (with dots), disp,
  * summary (+ optional blurred) for every env.  Equivalent to, per env:
  * indentation_from -> smooth_pyramid -> shade -> uint8 ; contact_center ->
@@ -170,6 +189,7 @@ typedef struct tac_pipeline_args {
   float* summary;           /* [N,8] out, nullable (tac_contact layout) */
   double* contact;          /* fp64 [N,8] out, nullable (tac_contact layout) */
   float* blurred;           /* [N,H,W] out, nullable (parity/debug) */
+  const float* shadow;      /* [N,H,W] shadow factor from tac_shadow, nullable (= no shadows) */
   int32_t splat;            /* nonzero: draw marker dots into rgb */
   void* workspace;
   int64_t n_env;

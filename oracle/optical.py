@@ -100,7 +100,7 @@ def lut_bins(gx, gy, g_max, n_mag, n_dir):
     return mb, db
 
 
-def shade_lut(blurred, pitch, lut, background, g_max):
+def shade_lut(blurred, pitch, lut, background, g_max, shadow=None):
     """Binned-LUT shading of a smoothed indentation map -> uint8 RGB.
 
     Builder's definition (SURVEY.md Appendix "Binned-LUT definition"):
@@ -109,6 +109,8 @@ def shade_lut(blurred, pitch, lut, background, g_max):
     basis_k(nx, ny) with the basis order of optical.py:82-88 (c0 cancels as in
     optical.py:244), then rgb = clip(rint(bg + Delta), 0, 255) with bg in
     8-bit units.  ``lut`` is (n_mag, n_dir, 3, 6), ``background`` (H, W, 3).
+    With ``shadow`` (H, W) the clipped shading is multiplied by it before
+    rounding (shade clips, optical.py:246; add_shadows multiplies, :299).
     Returns (rgb_u8, saturated_count).
     """
     lut = np.asarray(lut, dtype=np.float64)
@@ -120,7 +122,10 @@ def shade_lut(blurred, pitch, lut, background, g_max):
     coef = lut[mb, db]  # (..., H, W, 3, 6)
     basis = poly_basis(n[..., 0], n[..., 1], 2)  # (..., H, W, 6)
     delta = np.einsum("...ck,...k->...c", coef[..., 1:], basis[..., 1:])
-    raw = np.rint(np.asarray(background, dtype=np.float64) + delta)
+    val = np.asarray(background, dtype=np.float64) + delta
+    if shadow is not None:
+        val = np.clip(val, 0.0, 255.0) * np.asarray(shadow, dtype=np.float64)[..., None]
+    raw = np.rint(val)
     out = np.clip(raw, 0.0, 255.0)
     return out.astype(np.uint8), int((raw != out).sum())
 
@@ -131,3 +136,72 @@ def lut_from_global(coeffs, n_mag, n_dir, scale=255.0):
     to within 1 LSB (the only reference anchor of the binned LUT)."""
     c = np.asarray(coeffs, dtype=np.float64) * scale
     return np.broadcast_to(c, (n_mag, n_dir) + c.shape).copy()
+
+
+def shadow_offsets(direction, max_steps):
+    """Per-step pixel offsets (di, dj) of the march toward one light.
+
+    optical.py:283-291: lateral = hypot(lx, ly); dx, dy = lx/lateral,
+    ly/lateral; di = int(round(s*dy)), dj = int(round(s*dx)) (Python round =
+    half-to-even); rise_per_px = pitch * lz / lateral.  Returns None for an
+    overhead light (lateral < 1e-9), else (di[], dj[], lz / lateral).
+    """
+    lx, ly, lz = (float(v) for v in direction)
+    lateral = float(np.hypot(lx, ly))
+    if lateral < 1e-9:
+        return None
+    dx, dy = lx / lateral, ly / lateral
+    di = np.array([int(round(s * dy)) for s in range(1, max_steps + 1)])
+    dj = np.array([int(round(s * dx)) for s in range(1, max_steps + 1)])
+    return di, dj, lz / lateral
+
+
+def shadow_factor(elev, pitch, directions, factor=0.6, max_steps=80, softness=5e-5):
+    """Multiplicative shadow factor (H, W) of add_shadows, optical.py:261-300.
+
+    For each light: occ = max_s (elev[clip(i+di_s), clip(j+dj_s)] - elev -
+    s*rise), weight = clip(occ/softness, 0, 1), and the image is multiplied by
+    1 - (1 - factor) * weight; the product over lights is returned.  ``elev``
+    is the elevation (a HeightMap's -values).
+    """
+    e = np.asarray(elev, dtype=np.float64)
+    h, w = e.shape
+    out = np.ones_like(e)
+    if factor == 1.0:
+        return out
+    for d in directions:
+        off = shadow_offsets(d, max_steps)
+        if off is None:
+            continue
+        di, dj, rise = off
+        rise_per_px = pitch * rise
+        occ = np.full(e.shape, -np.inf)
+        for s in range(max_steps):
+            ii = np.clip(np.arange(h) + di[s], 0, h - 1)
+            jj = np.clip(np.arange(w) + dj[s], 0, w - 1)
+            np.maximum(occ, e[np.ix_(ii, jj)] - e - (s + 1) * rise_per_px, out=occ)
+        out = out * (1.0 - (1.0 - factor) * np.clip(occ / softness, 0.0, 1.0))
+    return out
+
+
+def add_shadows(rgb, elev, pitch, directions, factor=0.6, max_steps=80, softness=5e-5):
+    """rgb (H, W, 3) float times the per-light factors, applied light by light
+    in the reference order (optical.py:293-299)."""
+    img = np.array(rgb, dtype=np.float64, copy=True)
+    if factor == 1.0:
+        return img
+    e = np.asarray(elev, dtype=np.float64)
+    h, w = e.shape
+    for d in directions:
+        off = shadow_offsets(d, max_steps)
+        if off is None:
+            continue
+        di, dj, rise = off
+        rise_per_px = pitch * rise
+        occ = np.full(e.shape, -np.inf)
+        for s in range(max_steps):
+            ii = np.clip(np.arange(h) + di[s], 0, h - 1)
+            jj = np.clip(np.arange(w) + dj[s], 0, w - 1)
+            np.maximum(occ, e[np.ix_(ii, jj)] - e - (s + 1) * rise_per_px, out=occ)
+        img *= (1.0 - (1.0 - factor) * np.clip(occ / softness, 0.0, 1.0))[..., None]
+    return img

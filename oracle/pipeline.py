@@ -6,7 +6,7 @@ optical.py:281-282) and the marker-dot splat of marker.py:203-234 drawn on the
 quantised frame:
 
   depth -> indentation_from -> smooth_pyramid -> gradient/normals -> binned
-  LUT shade -> uint8 ; contact_center (raw indentation, envs.py:1177) ->
+  LUT shade (-> add_shadows when a shadow factor < 1 is given) -> uint8 ; contact_center (raw indentation, envs.py:1177) ->
   load (given shear/twist, or track_load) -> marker_displacements ->
   render_markers.
 """
@@ -33,11 +33,20 @@ def simulate_env(
     dot_radius=3,
     dot_color=(25, 25, 25),
     splat=True,
+    light_dirs=None,
+    shadow_factor=1.0,
+    shadow_steps=80,
+    shadow_softness=5e-5,
 ):
     """Returns dict(rgb u8 (H,W,3), disp (R,C,2), summary (8,), blurred (H,W))."""
     ind = tactile.indentation_from(depth, rest)
     blurred = tactile.smooth_pyramid(ind, levels)
-    rgb, _ = optical.shade_lut(blurred, pitch, lut, background, g_max)
+    shadow = None
+    if light_dirs is not None and len(light_dirs) and shadow_factor != 1.0:
+        # add_shadows on the height map (elevation = -depth), REF/envs.py:1173
+        shadow = optical.shadow_factor(-np.asarray(depth, dtype=np.float64), pitch, light_dirs,
+                                       shadow_factor, shadow_steps, shadow_softness)
+    rgb, _ = optical.shade_lut(blurred, pitch, lut, background, g_max, shadow)
     c = marker.contact_center(ind, pitch, threshold)
     load = dict(c)
     if c["in_contact"]:

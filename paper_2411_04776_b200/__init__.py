@@ -41,6 +41,8 @@ _LAZY = {
     "normals_from": ".optical",
     "shade": ".optical",
     "lut_from_polytable": ".optical",
+    "add_shadows": ".optical",
+    "shadow_factor": ".optical",
     "contact_center": ".marker",
     "track_load": ".marker",
     "marker_displacements": ".marker",

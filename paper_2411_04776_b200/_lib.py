@@ -20,6 +20,8 @@ TAC_ERR_CUDA = 2
 TAC_ERR_UNSUPPORTED = 3
 TAC_MAX_LEVELS = 8
 TAC_MAX_RADIUS = 24
+TAC_MAX_LIGHTS = 4
+TAC_MAX_SHADOW_STEPS = 256
 TAC_INPUT_DEPTH = 0
 TAC_INPUT_INDENTATION = 1
 TAC_LOAD_GIVEN = 0
@@ -55,6 +57,11 @@ class TacConfig(ctypes.Structure):
         ("contact_threshold", ctypes.c_double),
         ("dot_radius", _i32),
         ("dot_color", ctypes.c_uint8 * 3),
+        ("n_lights", _i32),
+        ("light_dir", (ctypes.c_double * 3) * TAC_MAX_LIGHTS),
+        ("shadow_factor", ctypes.c_double),
+        ("shadow_steps", _i32),
+        ("shadow_softness", ctypes.c_double),
     ]
 
 
@@ -72,6 +79,7 @@ class TacPipelineArgs(ctypes.Structure):
         ("summary", _p),
         ("contact", _p),
         ("blurred", _p),
+        ("shadow", _p),
         ("splat", _i32),
         ("workspace", _p),
         ("n_env", _i64),
@@ -93,6 +101,7 @@ SIGNATURES = {
     "tac_track_load": (ctypes.c_int, [_p, _p, _p, _p, _i64, _p]),
     "tac_marker_displacements": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
     "tac_render_markers": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
+    "tac_shadow": (ctypes.c_int, [_p, _p, _i32, _p, _p, _i64, _p]),
     "tac_pipeline": (ctypes.c_int, [_p, ctypes.POINTER(TacPipelineArgs), _p]),
 }
 

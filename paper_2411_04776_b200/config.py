@@ -123,6 +123,11 @@ class PipelineConfig:
     dot_radius: int = 3
     dot_color: Tuple[int, int, int] = (25, 25, 25)
     rest_grid: Optional[np.ndarray] = None
+    # add_shadows (REF/optical.py:261-300); factor 1.0 = off (the parity setting)
+    light_dirs: Optional[np.ndarray] = None  # (n_lights, 3), e.g. default_lighting().directions
+    shadow_factor: float = 1.0
+    shadow_steps: int = 80
+    shadow_softness: float = 5e-5
 
     def __post_init__(self):
         h, w = self.sensor.image_size
@@ -149,6 +154,16 @@ class PipelineConfig:
         if grid.shape != (self.sensor.marker_grid[0], self.sensor.marker_grid[1], 2):
             raise InvalidArgumentError("rest_positions must be (rows, cols, 2)")
         object.__setattr__(self, "rest_grid", grid)
+        if not 0.0 <= self.shadow_factor <= 1.0:
+            raise InvalidArgumentError("shadow factor must be in [0, 1]")
+        dirs = np.zeros((0, 3)) if self.light_dirs is None else np.asarray(self.light_dirs, np.float64)
+        if dirs.ndim != 2 or dirs.shape[1] != 3 or len(dirs) > 4:
+            raise InvalidArgumentError("light_dirs must be (n <= 4, 3)")
+        object.__setattr__(self, "light_dirs", dirs)
+
+    @property
+    def shadows(self) -> bool:
+        return self.shadow_factor != 1.0 and len(self.light_dirs) > 0
 
     @property
     def pixel_pitch(self):

@@ -80,6 +80,13 @@ class Context:
         c.dot_radius = int(cfg.dot_radius)
         for i in range(3):
             c.dot_color[i] = int(cfg.dot_color[i])
+        c.n_lights = len(cfg.light_dirs)
+        for l, d in enumerate(cfg.light_dirs):
+            for q in range(3):
+                c.light_dir[l][q] = float(d[q])
+        c.shadow_factor = float(cfg.shadow_factor)
+        c.shadow_steps = int(cfg.shadow_steps)
+        c.shadow_softness = float(cfg.shadow_softness)
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(self.lib.tac_ctx_create(ctypes.byref(c), ctypes.byref(handle)), "tac_ctx_create")

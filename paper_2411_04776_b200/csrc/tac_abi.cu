@@ -21,6 +21,9 @@ struct tac_ctx {
   float* d_bg = nullptr;
   uint8_t* d_bg_u8 = nullptr;
   double* d_grid = nullptr;
+  int2* d_shadow_off = nullptr;
+  float* d_shadow_cost = nullptr;
+  ShadowParams shadow;
   FrameParams fused, blur, contact;  // per-mode launch templates
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
@@ -87,6 +90,8 @@ int free_ctx(tac_ctx* c) {
   cudaFree(c->d_bg);
   cudaFree(c->d_bg_u8);
   cudaFree(c->d_grid);
+  cudaFree(c->d_shadow_off);
+  cudaFree(c->d_shadow_cost);
   delete c;
   return TAC_OK;
 }
@@ -153,6 +158,19 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   if (!std::isfinite(k.k_n) || !std::isfinite(k.k_t)) return fail(TAC_ERR_INVALID, "marker params must be finite");
   if (!finite_pos(k.contact_threshold)) return fail(TAC_ERR_INVALID, "threshold must be positive");
   if (k.dot_radius < 0 || k.dot_radius > 32) return fail(TAC_ERR_UNSUPPORTED, "dot_radius must be in 0..32");
+  if (k.n_lights < 0 || k.n_lights > TAC_MAX_LIGHTS)
+    return fail(TAC_ERR_INVALID, "n_lights must be in 0..%d", TAC_MAX_LIGHTS);
+  if (!(k.shadow_factor >= 0.0 && k.shadow_factor <= 1.0))
+    return fail(TAC_ERR_INVALID, "shadow factor must be in [0, 1]");
+  const bool shadows_on = k.shadow_factor != 1.0 && k.n_lights > 0;
+  if (shadows_on) {
+    if (k.shadow_steps < 1 || k.shadow_steps > TAC_MAX_SHADOW_STEPS)
+      return fail(TAC_ERR_UNSUPPORTED, "shadow steps must be in 1..%d", TAC_MAX_SHADOW_STEPS);
+    if (!finite_pos(k.shadow_softness)) return fail(TAC_ERR_INVALID, "shadow softness must be positive");
+    for (int l = 0; l < k.n_lights; ++l)
+      for (int q = 0; q < 3; ++q)
+        if (!std::isfinite(k.light_dir[l][q])) return fail(TAC_ERR_INVALID, "lighting values must be finite");
+  }
   const size_t HW = (size_t)k.height * k.width;
   for (size_t i = 0; i < HW * 3; ++i)
     if (!std::isfinite(k.background[i])) return fail(TAC_ERR_INVALID, "table values must be finite");
@@ -211,6 +229,55 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
       free_ctx(c);
       return cuda_fail(e, "context upload");
     }
+  }
+
+  // add_shadows march tables, exactly as REF/optical.py:283-291 in fp64
+  {
+    ShadowParams& sp = c->shadow;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.H = k.height;
+    sp.W = k.width;
+    std::vector<int2> off;
+    std::vector<float> cost;
+    int lights = 0;
+    if (shadows_on) {
+      for (int l = 0; l < k.n_lights; ++l) {
+        const double lx = k.light_dir[l][0], ly = k.light_dir[l][1], lz = k.light_dir[l][2];
+        const double lateral = std::hypot(lx, ly);
+        if (lateral < 1e-9) continue;  // overhead light casts no lateral shadow
+        const double dx = lx / lateral, dy = ly / lateral;
+        const double rise = k.pixel_pitch * lz / lateral;
+        for (int st = 1; st <= k.shadow_steps; ++st) {
+          int2 o;
+          o.x = (int)std::nearbyint(st * dy);  // Python round: half to even
+          o.y = (int)std::nearbyint(st * dx);
+          off.push_back(o);
+          cost.push_back((float)(st * rise));
+          sp.di_min = std::min(sp.di_min, o.x);
+          sp.di_max = std::max(sp.di_max, o.x);
+          sp.dj_min = std::min(sp.dj_min, o.y);
+          sp.dj_max = std::max(sp.dj_max, o.y);
+        }
+        ++lights;
+      }
+    }
+    sp.n_lights = lights;
+    sp.steps = lights ? k.shadow_steps : 0;
+    sp.one_minus_factor = (float)(1.0 - k.shadow_factor);
+    sp.inv_softness = shadows_on ? (float)(1.0 / k.shadow_softness) : 0.f;
+    if (lights) {
+      e = cudaMalloc(&c->d_shadow_off, off.size() * sizeof(int2));
+      if (e == cudaSuccess) e = cudaMemcpy(c->d_shadow_off, off.data(), off.size() * sizeof(int2), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaMalloc(&c->d_shadow_cost, cost.size() * sizeof(float));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(c->d_shadow_cost, cost.data(), cost.size() * sizeof(float), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) {
+        free_ctx(c);
+        return cuda_fail(e, "shadow tables");
+      }
+    }
+    sp.off = c->d_shadow_off;
+    sp.cost = c->d_shadow_cost;
   }
 
   MarkerGeom& mg = c->mg;
@@ -407,6 +474,18 @@ int tac_render_markers(const tac_ctx* c, const float* disp, uint8_t* rgb, int64_
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_render_markers");
 }
 
+int tac_shadow(const tac_ctx* c, const float* in, int32_t input_kind, float* factor, float* rgb,
+               int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (input_kind != TAC_INPUT_DEPTH && input_kind != TAC_INPUT_INDENTATION)
+    return fail(TAC_ERR_INVALID, "unknown input_kind %d", input_kind);
+  if (n_env && !in) return fail(TAC_ERR_INVALID, "null buffer");
+  cudaError_t e = launch_shadow(c->shadow, in, input_kind == TAC_INPUT_DEPTH, factor, rgb, n_env,
+                                (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_shadow");
+}
+
 int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   if (!a) return fail(TAC_ERR_INVALID, "null args");
   int st = common_checks(c, a->n_env);
@@ -440,6 +519,7 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   p.pose_delta = a->pose_delta;
   p.disp = a->disp;
   p.splat = a->splat;
+  p.shadow = a->shadow;
   bind_workspace(c, p, a->workspace, a->n_env);
   cudaError_t e = launch_frame(p, kModeFused, (cudaStream_t)stream);
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_pipeline");

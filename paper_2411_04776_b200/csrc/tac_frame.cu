@@ -436,6 +436,18 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
         gys[k] = (yb - yt) * sy;
       }
     }
+    float sf[4] = {1.f, 1.f, 1.f, 1.f};
+    const float* shadow = p.shadow;
+    if (shadow) {
+      const float* sp = shadow + g.env * (long long)p.H * p.W + (long long)y * p.W + xg;
+      if (vec_bg) {
+        const float4 f4 = __ldg(reinterpret_cast<const float4*>(sp));
+        sf[0] = f4.x; sf[1] = f4.y; sf[2] = f4.z; sf[3] = f4.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sf[k] = (xg + k < g.x1) ? __ldg(sp + k) : 1.f;
+      }
+    }
     uint32_t q[12];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -445,6 +457,11 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
       const float4 a1 = __ldg(p1.lut), c1 = __ldg(p1.lut + 1), d1 = __ldg(p1.lut + 2), e1 = __ldg(p1.lut + 3);
       float r = bgv[6 * h], gg = bgv[6 * h + 1], b = bgv[6 * h + 2];
       add_lut(a0, c0, d0, e0, p0.nx, p0.ny, r, gg, b);
+      if (shadow) {  // clip, then the multiplicative shadow (REF/optical.py:246, :299)
+        r = clampf(r, 0.f, 255.f) * sf[2 * h];
+        gg = clampf(gg, 0.f, 255.f) * sf[2 * h];
+        b = clampf(b, 0.f, 255.f) * sf[2 * h];
+      }
       q[6 * h] = u8sat(r);
       q[6 * h + 1] = u8sat(gg);
       q[6 * h + 2] = u8sat(b);
@@ -452,6 +469,11 @@ __device__ __forceinline__ void shade_rows(const FrameParams& p, const Geo& g, i
       gg = bgv[6 * h + 4];
       b = bgv[6 * h + 5];
       add_lut(a1, c1, d1, e1, p1.nx, p1.ny, r, gg, b);
+      if (shadow) {
+        r = clampf(r, 0.f, 255.f) * sf[2 * h + 1];
+        gg = clampf(gg, 0.f, 255.f) * sf[2 * h + 1];
+        b = clampf(b, 0.f, 255.f) * sf[2 * h + 1];
+      }
       q[6 * h + 3] = u8sat(r);
       q[6 * h + 4] = u8sat(gg);
       q[6 * h + 5] = u8sat(b);
@@ -877,7 +899,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kThreads + kShadeThreads 
           int nz = 0;
           for (int gr = max(y_lo - 1 - p.R, -p.R); gr <= min(y_hi + p.R, p.H + p.R - 1); ++gr)
             nz |= rownz[gr + p.R];
-          s_nz[b % kSlots] = nz;
+          s_nz[b % kSlots] = nz || p.shadow != nullptr;  // shadows reach flat regions
         }
         bar_arrive(kBarFull + b % kSlots, kThreads + kShadeThreads);
       } else {

@@ -89,7 +89,22 @@ struct FrameParams {
   const double* pose_delta;
   float* disp;           // nullable
   int splat;
+  const float* shadow;   // nullable [N][H][W] multiplicative shadow factor
 };
+
+// add_shadows march tables (REF/optical.py:283-299), built on the host.
+struct ShadowParams {
+  int H, W;
+  int n_lights, steps;
+  const int2* off;       // [n_lights * steps] (di, dj)
+  const float* cost;     // [n_lights * steps] s * pitch * lz / lateral
+  float one_minus_factor;
+  float inv_softness;
+  int di_min, di_max, dj_min, dj_max;  // offset bounds (interior fast path)
+};
+
+cudaError_t launch_shadow(const ShadowParams& s, const float* in, int input_depth, float* factor,
+                          float* rgb, long long n_env, cudaStream_t st);
 
 size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);

@@ -68,3 +68,68 @@ def lut_from_polytable(coeffs, mag_bins=125, dir_bins=180, scale=255.0) -> np.nd
 
         raise InvalidArgumentError("coeffs must be (3, 6) for degree 2")
     return np.broadcast_to((c * scale).astype(np.float32), (mag_bins, dir_bins, 3, 6)).copy()
+
+
+_SHADOW_CFGS = {}
+
+
+def _shadow_config(h, w, pitch, directions, factor, max_steps, softness):
+    from .config import SensorConfig
+
+    dirs = np.asarray(directions, dtype=np.float64)
+    key = (h, w, float(pitch), dirs.tobytes(), float(factor), int(max_steps), float(softness))
+    cfg = _SHADOW_CFGS.get(key)
+    if cfg is None:
+        cfg = PipelineConfig(
+            sensor=SensorConfig.from_pitch(h, w, pitch), levels=((0.0, 0),),
+            lut=np.zeros((1, 1, 3, 6), np.float32), background=np.zeros((h, w, 3), np.float32),
+            light_dirs=dirs, shadow_factor=factor, shadow_steps=max_steps, shadow_softness=softness,
+        )
+        _SHADOW_CFGS[key] = cfg
+    return cfg
+
+
+def shadow_factor(hm: HeightMap, directions, factor=0.6, max_steps=80, softness=5e-5) -> torch.Tensor:
+    """Multiplicative shadow factor [N, H, W] of add_shadows (REF/optical.py:261-300)
+    for the light directions (n, 3) (e.g. a LightingModel's ``directions``)."""
+    from .errors import InvalidArgumentError
+
+    if not 0.0 <= factor <= 1.0:
+        raise InvalidArgumentError("shadow factor must be in [0, 1]")
+    v = hm.values
+    single = v.dim() == 2
+    v = (v.unsqueeze(0) if single else v).contiguous().float()
+    n, h, w = v.shape
+    cfg = _shadow_config(h, w, hm.pixel_pitch, directions, factor, max_steps, softness)
+    ctx = context_for(cfg, v.device)
+    out = torch.empty((n, h, w), dtype=torch.float32, device=v.device)
+    if not cfg.shadows:
+        out.fill_(1.0)
+    else:
+        _lib.check(ctx.lib.tac_shadow(ctx.handle, v.data_ptr(), _lib.TAC_INPUT_DEPTH, out.data_ptr(), None, n,
+                                      ctx.stream()), "tac_shadow")
+    return out[0] if single else out
+
+
+def add_shadows(rgb, hm: HeightMap, directions, factor=0.6, max_steps=80, softness=5e-5) -> torch.Tensor:
+    """Mirror of add_shadows (REF/optical.py:261-300): returns a darkened copy of
+    the float RGB [N, H, W, 3] (or [H, W, 3]); factor 1.0 is the identity."""
+    from .errors import InvalidArgumentError
+
+    if not 0.0 <= factor <= 1.0:
+        raise InvalidArgumentError("shadow factor must be in [0, 1]")
+    img = rgb.detach().clone().float().contiguous()
+    single = img.dim() == 3
+    if single:
+        img = img.unsqueeze(0)
+    v = hm.values
+    v = (v.unsqueeze(0) if v.dim() == 2 else v).contiguous().float()
+    if tuple(img.shape[:3]) != tuple(v.shape):
+        raise InvalidArgumentError("image and height map shapes differ")
+    n, h, w = v.shape
+    cfg = _shadow_config(h, w, hm.pixel_pitch, directions, factor, max_steps, softness)
+    if cfg.shadows:
+        ctx = context_for(cfg, v.device)
+        _lib.check(ctx.lib.tac_shadow(ctx.handle, v.data_ptr(), _lib.TAC_INPUT_DEPTH, None, img.data_ptr(), n,
+                                      ctx.stream()), "tac_shadow")
+    return img[0] if single else img

@@ -10,7 +10,7 @@ from paper_2411_04776_b200.config import MarkerParams, PipelineConfig, SensorCon
 
 
 def small_config(h=48, w=64, grid=(5, 7), sigmas=(1.0, 2.0, 4.0), seed=0, bins=(125, 180),
-                 lambda_n=0.8e-3, dot_radius=3, pitch=synthetic.PITCH, levels=None):
+                 lambda_n=0.8e-3, dot_radius=3, pitch=synthetic.PITCH, levels=None, shadows=False):
     return PipelineConfig(
         sensor=SensorConfig.from_pitch(h, w, pitch, synthetic.REST, grid),
         levels=levels if levels is not None else levels_from_sigmas(sigmas),
@@ -19,7 +19,22 @@ def small_config(h=48, w=64, grid=(5, 7), sigmas=(1.0, 2.0, 4.0), seed=0, bins=(
         g_max=1.0,
         marker_params=MarkerParams(lambda_n=lambda_n),
         dot_radius=dot_radius,
+        light_dirs=DEFAULT_LIGHT_DIRS if shadows else None,
+        shadow_factor=0.6 if shadows else 1.0,
     )
+
+
+# tacsim default_lighting() directions (REF/optical.py:68-79): R, G, B lights
+# 120 degrees apart in azimuth at 35 degrees elevation, normalised as
+# LightingModel does (REF/optical.py:36-45).
+def _default_dirs():
+    el = np.deg2rad(35.0)
+    az = np.deg2rad([0.0, 120.0, 240.0])
+    d = np.stack([np.cos(el) * np.cos(az), np.cos(el) * np.sin(az), np.full(3, np.sin(el))], axis=1)
+    return d / np.linalg.norm(d, axis=-1, keepdims=True)
+
+
+DEFAULT_LIGHT_DIRS = _default_dirs()
 
 
 def depth_batch(n, h, w, seed, pitch=synthetic.PITCH, **kw):
@@ -46,6 +61,10 @@ def oracle_env(cfg: PipelineConfig, depth_f32, shear, twist, splat=True):
         dot_radius=cfg.dot_radius,
         dot_color=cfg.dot_color,
         splat=splat,
+        light_dirs=cfg.light_dirs,
+        shadow_factor=cfg.shadow_factor,
+        shadow_steps=cfg.shadow_steps,
+        shadow_softness=cfg.shadow_softness,
     )
 
 

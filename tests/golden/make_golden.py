@@ -105,6 +105,23 @@ def optical_cases(tact):
     )
 
 
+def shadow_cases(tact, opt):
+    """add_shadows (optical.py:261-300) on the press maps, default lighting and
+    a single grazing light, factor 0.6 and 0.3."""
+    lights = op.default_lighting()
+    graze = op.LightingModel(np.array([[0.94, 0.0, 0.34]] * 3), np.eye(3), np.zeros(3))
+    bumpy = np.full((H, W), REST)
+    bumpy[20:26, 30:36] = REST - 1e-3
+    maps = np.stack([tact["depth"][0], bumpy, tact["depth"][2]])
+    rgb = opt["shaded"][0]
+    out = dict(maps=maps, rgb=rgb, dirs_default=lights.directions, dirs_graze=graze.directions)
+    for mi, hmv in enumerate(maps):
+        hm = tac.HeightMap(hmv, PITCH)
+        out[f"default_{mi}"] = op.add_shadows(rgb, hm, lights)
+        out[f"graze_{mi}"] = op.add_shadows(rgb, hm, graze, factor=0.3, max_steps=40, softness=2e-5)
+    return out
+
+
 def marker_cases(tact, opt):
     rng = np.random.default_rng(99)
     grid = mk.grid_rest_positions(CFG)
@@ -182,10 +199,12 @@ def main():
     tact = tactile_cases()
     opt = optical_cases(tact)
     mark = marker_cases(tact, opt)
+    shad = shadow_cases(tact, opt)
+    np.savez_compressed(os.path.join(OUT, "shadows.npz"), **shad)
     np.savez_compressed(os.path.join(OUT, "tactile.npz"), **tact)
     np.savez_compressed(os.path.join(OUT, "optical.npz"), **opt)
     np.savez_compressed(os.path.join(OUT, "marker.npz"), **mark)
-    for name in ("tactile", "optical", "marker"):
+    for name in ("tactile", "optical", "marker", "shadows"):
         p = os.path.join(OUT, f"{name}.npz")
         print(p, os.path.getsize(p))
 

@@ -388,3 +388,52 @@ class TestBoundaryErrors:
 
         with pytest.raises(UnsupportedConfigError):
             smooth_pyramid(IndentationMap(torch.zeros((64, 64), device=DEV), 1e-5), [51])
+
+
+class TestShadows:
+    """Row f1: add_shadows (REF/optical.py:261-300) on the GPU."""
+
+    def test_mirror_against_reference_golden(self, golden):
+        from paper_2411_04776_b200 import add_shadows
+
+        g = golden("shadows")
+        rgb = torch.as_tensor(g["rgb"], dtype=torch.float32, device=DEV)
+        for mi, hmv in enumerate(g["maps"]):
+            hm = HeightMap(torch.as_tensor(hmv, dtype=torch.float32, device=DEV), 2.66e-5)
+            out = add_shadows(rgb, hm, g["dirs_default"]).cpu().numpy()
+            assert np.abs(out - g[f"default_{mi}"]).max() < 1e-4, mi
+            out = add_shadows(rgb, hm, g["dirs_graze"], factor=0.3, max_steps=40, softness=2e-5).cpu().numpy()
+            assert np.abs(out - g[f"graze_{mi}"]).max() < 1e-4, mi
+
+    def test_factor_one_is_identity(self, golden):
+        from paper_2411_04776_b200 import add_shadows
+
+        g = golden("shadows")
+        rgb = torch.as_tensor(g["rgb"], dtype=torch.float32, device=DEV)
+        hm = HeightMap(torch.as_tensor(g["maps"][1], dtype=torch.float32, device=DEV), 2.66e-5)
+        assert torch.equal(add_shadows(rgb, hm, g["dirs_default"], factor=1.0), rgb)
+
+    def test_factor_matches_oracle_on_batches(self):
+        from paper_2411_04776_b200 import shadow_factor
+
+        from _helpers import DEFAULT_LIGHT_DIRS
+
+        depth = depth_batch(4, 96, 128, seed=41)
+        f = shadow_factor(HeightMap(depth.to(DEV), synthetic.PITCH), DEFAULT_LIGHT_DIRS).cpu().numpy()
+        for i in range(4):
+            ref = oop.shadow_factor(-depth[i].numpy().astype(np.float64), synthetic.PITCH, DEFAULT_LIGHT_DIRS)
+            assert np.abs(f[i] - ref).max() < 1e-4
+
+    @pytest.mark.parametrize("hw", [(48, 64), (240, 320), (61, 130)])
+    def test_pipeline_with_shadows(self, hw):
+        h, w = hw
+        cfg = small_config(h, w, shadows=True)
+        depth = depth_batch(6, h, w, seed=43)
+        shear, twist = synthetic.loads(6, 44)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        worst = 1.0
+        for i in range(6):
+            ref = oracle_env(cfg, depth[i].numpy(), shear[i], twist[i])
+            mx, frac = rgb_stats(obs.rgb[i].cpu().numpy(), ref["rgb"])
+            worst = min(worst, frac)
+        assert worst >= RGB_FRAC

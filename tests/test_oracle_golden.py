@@ -134,3 +134,28 @@ class TestMarkerGolden:
         grey = np.full((48, 64, 3), 230, np.uint8)
         img4 = marker.render_markers(grey, pos, 2.66e-5, 4)
         assert np.array_equal(img4, g["render_r4_grey"])
+
+
+class TestShadowsGolden:
+    """add_shadows (optical.py:261-300) restated: per-light march, soft edge,
+    multiplicative factor; pinned on the reference's own outputs."""
+
+    def test_default_and_grazing_lights(self, golden):
+        g = golden("shadows")
+        for mi, hm in enumerate(g["maps"]):
+            out = optical.add_shadows(g["rgb"], -hm, 2.66e-5, g["dirs_default"])
+            assert np.abs(out - g[f"default_{mi}"]).max() < 1e-12
+            out = optical.add_shadows(g["rgb"], -hm, 2.66e-5, g["dirs_graze"], factor=0.3,
+                                      max_steps=40, softness=2e-5)
+            assert np.abs(out - g[f"graze_{mi}"]).max() < 1e-12
+
+    def test_factor_form_matches(self, golden):
+        g = golden("shadows")
+        hm = g["maps"][1]
+        f = optical.shadow_factor(-hm, 2.66e-5, g["dirs_default"])
+        assert np.abs(g["rgb"] * f[..., None] - g["default_1"]).max() < 1e-12
+        assert (f < 1).any() and (f == 1).any()
+
+    def test_flat_map_identity(self, golden):
+        g = golden("shadows")
+        assert np.array_equal(g["default_2"], g["rgb"])
