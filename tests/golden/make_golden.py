@@ -195,16 +195,69 @@ def marker_cases(tact, opt):
     return out
 
 
+def render_cases():
+    """`tacsim calibrate` + `tacsim render` (REF/cli.py:274-319) run end to end
+    on four 480x640 TAC1 maps: flat, sphere presses of 0.4 and 0.8 mm (as
+    REF/tests/test_cli.py:148-161) and an off-centre cylinder."""
+    import contextlib
+    import io
+    import tempfile
+
+    import tacsim.cli as cli
+
+    cfg = tac.SensorConfig()
+    h, w = cfg.image_size
+    p, th = cfg.pixel_pitch, cfg.gelpad_thickness
+    yy, xx = np.mgrid[0:h, 0:w]
+    x = (xx + 0.5 - 0.5 * w) * p
+    y = (yy + 0.5 - 0.5 * h) * p
+
+    def press(depth, r=5e-3, cx=0.0, cy=0.0):
+        rho2 = (x - cx) ** 2 + (y - cy) ** 2
+        sph = th - depth + r - np.sqrt(np.maximum(0.0, r * r - rho2))
+        return np.where(rho2 <= r * r, np.minimum(np.full((h, w), th), sph), th)
+
+    perp = (x - 1e-3) * np.sin(0.4) - (y + 5e-4) * np.cos(0.4)
+    cyl = np.where(np.abs(perp) < 3e-3, th - np.maximum(0.0, 6e-4 - 3e-3 + np.sqrt(np.maximum(0, 9e-6 - perp * perp))), th)
+    maps = [np.full((h, w), th), press(4e-4), press(8e-4, cx=2e-3, cy=-1e-3), np.minimum(cyl, th)]
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        files = []
+        for i, m in enumerate(maps):
+            f = os.path.join(d, f"m{i}.raw")
+            tac.save_heightmap_raw(f, tac.HeightMap(m, p))
+            files.append(f)
+            out[f"raw_{i}"] = np.frombuffer(open(f, "rb").read(), dtype=np.uint8)
+        cal = os.path.join(d, "cal")
+        with contextlib.redirect_stdout(io.StringIO()):
+            assert cli.main(["calibrate", "--out", cal]) == 0
+        buf = io.StringIO()
+        rd = os.path.join(d, "r")
+        with contextlib.redirect_stdout(buf):
+            assert cli.main(["render", *files, "--table", os.path.join(cal, "table.json"),
+                             "--table-png", os.path.join(cal, "table.png"), "--out", rd]) == 0
+        out["table_json"] = np.frombuffer(open(os.path.join(cal, "table.json"), "rb").read(), dtype=np.uint8)
+        out["table_png"] = np.frombuffer(open(os.path.join(cal, "table.png"), "rb").read(), dtype=np.uint8)
+        out["counts"] = np.array([int(l.rsplit(" ", 1)[1]) for l in buf.getvalue().strip().split("\n")])
+        for i in range(len(maps)):
+            out[f"png_{i}"] = cv2.imread(os.path.join(rd, f"m{i}_tactile.png"))[:, :, ::-1]
+            field = mk.load_markers_csv(os.path.join(rd, f"m{i}_markers.csv"))
+            out[f"disp_{i}"] = field.displacements
+            out[f"rest_{i}"] = field.rest_positions
+    return out
+
+
 def main():
     tact = tactile_cases()
     opt = optical_cases(tact)
     mark = marker_cases(tact, opt)
     shad = shadow_cases(tact, opt)
     np.savez_compressed(os.path.join(OUT, "shadows.npz"), **shad)
+    np.savez_compressed(os.path.join(OUT, "render.npz"), **render_cases())
     np.savez_compressed(os.path.join(OUT, "tactile.npz"), **tact)
     np.savez_compressed(os.path.join(OUT, "optical.npz"), **opt)
     np.savez_compressed(os.path.join(OUT, "marker.npz"), **mark)
-    for name in ("tactile", "optical", "marker", "shadows"):
+    for name in ("tactile", "optical", "marker", "shadows", "render"):
         p = os.path.join(OUT, f"{name}.npz")
         print(p, os.path.getsize(p))
 
