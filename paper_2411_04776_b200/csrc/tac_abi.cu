@@ -25,6 +25,13 @@ struct tac_ctx {
   float* d_shadow_cost = nullptr;
   ShadowParams shadow;
   FrameParams fused, blur, contact;  // per-mode launch templates
+  FrameParams fused4;                // slot-ring fused kernel geometry
+  bool use4;                         // fused4 is eligible (TAC_FRAME=4 selects it)
+  FrameParams fused5;                // band-tiled two-kernel geometry (default)
+  bool use5;
+  long long chunk5;                  // envs per v5 launch pair
+  long long* prof = nullptr;         // diagnostics buffer (tac_set_profile_buffer)
+  long long prof_envs = 0;
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
 };
@@ -82,6 +89,65 @@ void plan_strips(FrameParams& p, int mode, int max_strip) {
   p.b_pitch = bp;
   (void)0;
   p.stage_bytes = (RB + 1) * p.strip_w * 3;
+}
+
+// Geometry of the slot-ring fused kernel (see tac_frame4.cu): vb rows start at
+// column bx0 - round_up(R, 4) and are read as 16-column chunks (+/- RL4).
+void plan_v4(FrameParams& p) {
+  const int R4 = round_up(p.R, 4);
+  const int ring = p.strips > 1 ? 1 : 0;
+  const int ew = p.strip_w + 2 * ring + 3;
+  const int nch = (ew + 15) / 16;
+  int vp = round_up(16 * nch + 2 * R4 + 4, 4);
+  if (((vp / 4) & 1) == 0) vp += 4;  // 4 x odd: LDS.128 over 8 rows is conflict-free
+  p.v_pitch = vp;
+  int bp = round_up(ew + 16 + 4, 4);
+  if (((bp / 4) & 1) == 0) bp += 4;
+  p.b_pitch = bp;
+  p.in_rows = 3 * RB;  // input slot ring of blocks b-1..b+1
+  p.stage_bytes = 0;
+}
+
+// Geometry of the band-tiled path (see tac_frame5.cu): input rows of W floats,
+// vb rows from column -round_up(R, 4) to W + round_up(R, 4).
+void plan_v5(FrameParams& p) {
+  const int R4 = round_up(p.R, 4);
+  p.bands = (p.H + 15) / 16;
+  p.in_pitch = p.W;
+  p.in_rows = 16 + 2 * p.R;
+  int vp = round_up(p.W + 2 * R4 + 4, 4);
+  if (((vp / 4) & 1) == 0) vp += 4;  // 4 x odd: LDS.128 over 8 rows is conflict-free
+  p.v_pitch = vp;
+  p.b_pitch = 0;
+  p.stage_bytes = 0;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// v5 workspace (after the v3 region): band partials for every env, then the
+// per-chunk band extents and blurred scratch.
+size_t v5_workspace_bytes(const tac_ctx* c, int64_t n_env) {
+  if (!c->use5) return 0;
+  const long long C = std::min<long long>(n_env, c->chunk5);
+  const FrameParams& p = c->fused5;
+  return align256((size_t)n_env * p.bands * kSumFields * sizeof(double)) +
+         align256((size_t)C * p.bands * sizeof(int2)) + align256((size_t)C * p.H * p.W * sizeof(float));
+}
+
+size_t v3_workspace_bytes(const tac_ctx* c, int64_t n_env) {
+  const size_t part = align256((size_t)n_env * c->max_tiles * kSumFields * sizeof(double));
+  return part + align256((size_t)n_env * sizeof(unsigned int));
+}
+
+void bind_workspace5(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) {
+  const long long C = std::min<long long>(n_env, c->chunk5);
+  char* b = reinterpret_cast<char*>(ws) + v3_workspace_bytes(c, n_env);
+  p.partials = reinterpret_cast<double*>(b);
+  b += align256((size_t)n_env * p.bands * kSumFields * sizeof(double));
+  p.band_ext = reinterpret_cast<int2*>(b);
+  b += align256((size_t)C * p.bands * sizeof(int2));
+  p.scratch = reinterpret_cast<float*>(b);
+  p.chunk = C;
 }
 
 int free_ctx(tac_ctx* c) {
@@ -323,6 +389,10 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
     for (int i = 0; i <= r; ++i) {
       b.wv[l][i] = (float)w[i];
       b.wh[l][i] = (float)(w[i] / k.n_levels);
+      if (i <= 16) {
+        b.wv2[l][i] = make_float2(b.wv[l][i], b.wv[l][i]);
+        b.wh2[l][i] = make_float2(b.wh[l][i], b.wh[l][i]);
+      }
     }
   }
   b.rest = (float)k.gel_thickness;
@@ -349,6 +419,14 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   c->contact = b;
   plan_strips(c->contact, kModeContact, max_strip);
   c->max_tiles = std::max({c->fused.strips, c->blur.strips, c->contact.strips});
+  c->fused4 = c->fused;
+  plan_v4(c->fused4);
+  const int kind = env_int("TAC_FRAME", 5);
+  c->use4 = kind == 4 && frame4_eligible(c->fused4);
+  c->fused5 = c->fused;
+  plan_v5(c->fused5);
+  c->use5 = kind == 5 && frame5_eligible(c->fused5);
+  c->chunk5 = std::max(1, env_int("TAC_CHUNK", 256));
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
     if (p.stage_bytes > (int)(RB * p.v_pitch * sizeof(float))) {
@@ -370,11 +448,18 @@ int tac_ctx_destroy(tac_ctx* ctx) { return free_ctx(ctx); }
 
 size_t tac_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   if (!c || n_env < 0) return 0;
-  const size_t part = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(double)) + 255) & ~size_t(255);
-  return part + (((size_t)n_env * sizeof(unsigned int) + 255) & ~size_t(255));
+  return v3_workspace_bytes(c, n_env) + v5_workspace_bytes(c, n_env);
 }
 
 int32_t tac_tiles_per_frame(const tac_ctx* c) { return c ? c->fused.strips : 0; }
+
+int tac_set_profile_buffer(tac_ctx* c, int64_t* buf, int64_t n_env) {
+  if (!c) return fail(TAC_ERR_INVALID, "null context");
+  if (n_env < 0 || (n_env > 0 && !buf)) return fail(TAC_ERR_INVALID, "bad profile buffer");
+  c->prof = n_env > 0 ? reinterpret_cast<long long*>(buf) : nullptr;
+  c->prof_envs = n_env;
+  return TAC_OK;
+}
 
 int tac_indentation(const tac_ctx* c, const float* depth, float* ind, int64_t n_env, void* stream) {
   int st = common_checks(c, n_env);
@@ -503,8 +588,13 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
     return fail(TAC_ERR_INVALID, "unknown load_mode %d", a->load_mode);
   }
   FrameParams p = c->fused;
+  const bool tma = tma_ok(p, a->in);
+  const bool v4 = c->use4 && tma;
+  const bool v5 = c->use5 && tma;
+  if (v4) p = c->fused4;
+  if (v5) p = c->fused5;
   p.in = a->in;
-  p.use_tma = tma_ok(p, a->in);
+  p.use_tma = tma;
   p.input_depth = a->input_kind == TAC_INPUT_DEPTH;
   p.rgb = a->rgb;
   p.blurred = a->blurred;
@@ -520,8 +610,16 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   p.disp = a->disp;
   p.splat = a->splat;
   p.shadow = a->shadow;
-  bind_workspace(c, p, a->workspace, a->n_env);
-  cudaError_t e = launch_frame(p, kModeFused, (cudaStream_t)stream);
+  p.prof = c->prof;
+  p.prof_envs = c->prof_envs;
+  cudaError_t e;
+  if (v5) {
+    bind_workspace5(c, p, a->workspace, a->n_env);
+    e = launch_frame5(p, (cudaStream_t)stream);
+  } else {
+    bind_workspace(c, p, a->workspace, a->n_env);
+    e = v4 ? launch_frame4(p, (cudaStream_t)stream) : launch_frame(p, kModeFused, (cudaStream_t)stream);
+  }
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_pipeline");
 }
 

@@ -1,0 +1,520 @@
+// Band-tiled two-kernel path (v5), the default tac_pipeline path for frames of
+// one strip (W <= 320, W % 16 == 0) with pyramid radii <= 16.
+//
+// Why two kernels: in the fused warp-specialised kernels (tac_frame.cu,
+// tac_frame4.cu) both the blur and the shade group run ~2.5 warps per SMSP
+// and every row block waits on the slower group; per-block clock stamps
+// (tools/phase_clock.py) showed both groups latency-bound at ~0.3 IPC.  Here
+// each stage gets the occupancy it needs:
+//
+//  band_blur_kernel   kernel (a): one CTA per (env, 16-row band), 3 CTAs/SM.
+//     TMA (cp.async.bulk, clamped row index = replicate border,
+//     REF/tactile.py:219-221) loads the band's 16 + 2R depth rows; the
+//     conversion pass clamps them (REF/tactile.py:193-197), folds the contact
+//     partials of REF/marker.py:109-121 (own rows only) and the band's
+//     non-zero column extent; then per level a vertical pass (column pair x 8
+//     rows per thread) and a horizontal pass (one row x 16 columns per thread,
+//     summed over levels in registers) write the blurred band to HBM/L2 with
+//     16-B stores.  Columns farther than R from any non-zero input are exactly
+//     0 and are not convolved (exact skip).
+//
+//  band_shade_kernel  kernel (b): 4 pixels per thread, ~40 warps per SM.  np.gradient differences (REF/optical.py:160), bins, binned-LUT
+//     shading (REF/optical.py:82-88, :244) + background, uint8 rule
+//     (REF/cli.py:134-139).  Pixels whose 3x3 blurred neighbourhood is zero
+//     (outside the band extents) are exactly rint(background) and copied.
+//
+//  env_epilogue_kernel  kernel (c): per env, reduces the band contact partials
+//     in a fixed order, finalises contact / summary / load
+//     (REF/marker.py:103-140), the marker displacements (REF/marker.py:143-165)
+//     and the dot splat (REF/marker.py:203-234).
+//
+// Envs run in chunks (TAC_CHUNK, default 256) so the blurred intermediate of a
+// chunk (256 x 307 KB = 79 MB at 240x320) stays resident in the 126 MB L2.
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tac_frame_common.cuh"
+
+namespace tac {
+
+namespace {
+
+constexpr int BH = 16;    // band rows
+constexpr int K1T = 320;  // blur threads: 16 rows x 20 chunks of 16 columns
+constexpr int K2T = 320;  // shade threads
+
+// Vertical pass, one column pair x 8 output rows of one level.  `src` = input
+// row (first output row - RL), column c; every load feeds up to 8 FFMA2.
+template <int RL>
+__device__ __forceinline__ void v5item(const float2* __restrict__ w, const float* __restrict__ src,
+                                       int ip, float* __restrict__ dst, int vp, bool st_y) {
+  float2 acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < 8 + 2 * RL; ++j) {
+    const float2 v = *reinterpret_cast<const float2*>(src + j * ip);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = j - k - RL;
+      if (t >= -RL && t <= RL) acc[k] = ffma2(w[t < 0 ? -t : t], v, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (st_y)
+      *reinterpret_cast<float2*>(dst + k * vp) = acc[k];
+    else
+      dst[k * vp] = acc[k].x;
+  }
+}
+
+// Horizontal pass, one row x 16 columns (8 column pairs) of one level, fast
+// path: the window [c0 - RL4, c0 + 16 + RL4) lies inside the computed vb
+// columns; `src` = vb row at column c0 - RL4 (16-B aligned).
+template <int RL>
+__device__ __forceinline__ void h5fast(const float2* __restrict__ w, const float* __restrict__ src,
+                                       float2 acc[8]) {
+  constexpr int RL4 = (RL + 3) & ~3;
+  constexpr int NV = 16 + 2 * RL4;
+  float v[NV];
+#pragma unroll
+  for (int q = 0; q < NV / 4; ++q) {
+    const float4 f = *reinterpret_cast<const float4*>(src + 4 * q);
+    v[4 * q] = f.x;
+    v[4 * q + 1] = f.y;
+    v[4 * q + 2] = f.z;
+    v[4 * q + 3] = f.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int t = -RL; t <= RL; ++t) {
+      const int a = RL4 + 2 * i + t;
+      acc[i] = ffma2(w[t < 0 ? -t : t], make_float2(v[a], v[a + 1]), acc[i]);
+    }
+  }
+}
+
+// Frame-border chunks: the window leaves the frame; column indices are
+// clamped (replicate border, scipy mode="nearest").  Same FFMA2 body.
+template <int RL>
+__device__ __forceinline__ void h5edge(const float2* __restrict__ w, const float* __restrict__ row0,
+                                       int c0, int W, float2 acc[8]) {
+  constexpr int RL4 = (RL + 3) & ~3;
+  constexpr int NV = 16 + 2 * RL4;
+  float v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = row0[min(max(c0 - RL4 + i, 0), W - 1)];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int t = -RL; t <= RL; ++t) {
+      const int a = RL4 + 2 * i + t;
+      acc[i] = ffma2(w[t < 0 ? -t : t], make_float2(v[a], v[a + 1]), acc[i]);
+    }
+  }
+}
+
+#define TAC5_RADIUS_CASES(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// kernel (a): clamp + contact partials + pyramid blur of one 16-row band.
+// grid (bands, envs); block (W/4, 320/(W/4)): threadIdx.x = float4 column group
+#ifndef TAC_K1_MINB
+#define TAC_K1_MINB 3
+#endif
+__global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __grid_constant__ FrameParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nb = p.bands;
+  const long long env = blockIdx.y;
+  const int band = blockIdx.x;
+  const int y0 = band * BH;
+  const int R = p.R;
+  const int R4 = (R + 3) & ~3;
+  const int nrows = BH + 2 * R;
+  const int W = p.W, H = p.H;
+  const long long HW = (long long)H * W;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int ip = p.in_pitch, vp = p.v_pitch;
+  const int vbase = -R4;  // column of vb index 0
+
+  float* inb = reinterpret_cast<float*>(smem_raw);  // nrows x ip (input row i = global row y0 - R + i)
+  float* vb = inb + nrows * ip;                     // BH x vp
+  __shared__ double s_red[(K1T / 32) * 8];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ int s_lo, s_hi;
+
+  const float* src = p.in + env * HW;
+  const unsigned row_bytes = (unsigned)W * 4u;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_lo = INT_MAX;
+    s_hi = INT_MIN;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&s_bar, row_bytes * (unsigned)nrows);
+    for (int i = 0; i < nrows; ++i) {
+      const int cr = min(max(y0 - R + i, 0), H - 1);
+      bulk_g2s(inb + i * ip, src + (long long)cr * W, row_bytes, &s_bar);
+    }
+  }
+
+  // ---- conversion: float4 groups, thread -> fixed column group ----------------
+  // rows [0, R) and [R + BH, nrows) are halo (clamp + extent only); rows
+  // [R, R + BH) are the band's own rows (+ contact partials).
+  Red red = red_zero();
+  float colsum[4] = {0.f, 0.f, 0.f, 0.f};
+  const int cg = threadIdx.x, ro = threadIdx.y, cstep = blockDim.y;
+  mbar_wait(&s_bar, 0);
+  bool nz = false;
+  auto clamp4 = [&](float4* e) -> float4 {
+    float4 v = *e;
+    if (p.input_depth) {
+      v.x = clampf((p.rest - v.x) + p.rest_lo, 0.f, p.rest);
+      v.y = clampf((p.rest - v.y) + p.rest_lo, 0.f, p.rest);
+      v.z = clampf((p.rest - v.z) + p.rest_lo, 0.f, p.rest);
+      v.w = clampf((p.rest - v.w) + p.rest_lo, 0.f, p.rest);
+      *e = v;
+    }
+    nz |= (v.x != 0.f) | (v.y != 0.f) | (v.z != 0.f) | (v.w != 0.f);
+    return v;
+  };
+  for (int i = ro; i < R; i += cstep) clamp4(reinterpret_cast<float4*>(inb + i * ip) + cg);
+  for (int i = R + BH + ro; i < nrows; i += cstep) clamp4(reinterpret_cast<float4*>(inb + i * ip) + cg);
+  const int own_rows = min(BH, H - y0);
+  for (int i = ro; i < own_rows; i += cstep) {
+    float4* e = reinterpret_cast<float4*>(inb + (R + i) * ip) + cg;
+    const float4 raw = *e;
+    // non-finite inputs are counted, not raised (summary field 6); the sum of
+    // four finite depths (metres) cannot overflow
+    if (!(fabsf(raw.x + raw.y + raw.z + raw.w) < INFINITY)) {
+      red.nf += (fabsf(raw.x) < INFINITY ? 0.f : 1.f) + (fabsf(raw.y) < INFINITY ? 0.f : 1.f) +
+                (fabsf(raw.z) < INFINITY ? 0.f : 1.f) + (fabsf(raw.w) < INFINITY ? 0.f : 1.f);
+    }
+    const float4 c4 = clamp4(e);
+    const float v[4] = {c4.x, c4.y, c4.z, c4.w};
+    float rowsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      red.mx = fmaxf(red.mx, v[k]);
+      const bool in = v[k] > p.threshold;
+      const float w = in ? v[k] : 0.f;
+      red.cnt += in ? 1.f : 0.f;
+      colsum[k] += w;
+      rowsum += w;
+    }
+    red.sw += (double)rowsum;
+    red.swy = fma((double)rowsum, (double)(y0 + i) + 0.5 - (double)p.half_h, red.swy);
+  }
+  {
+    const int c = 4 * cg;
+    const int lo = __reduce_min_sync(0xffffffffu, nz ? c : INT_MAX);
+    const int hi = __reduce_max_sync(0xffffffffu, nz ? c + 3 : INT_MIN);
+    if ((tid & 31) == 0 && lo != INT_MAX) {
+      atomicMin(&s_lo, lo);
+      atomicMax(&s_hi, hi);
+    }
+  }
+  __syncthreads();
+  const int ea = s_lo, eb = s_hi;
+
+  // ---- blur: output range [ha, hb] in whole 16-column chunks ------------------
+  const int nch = W >> 4;
+  int k_lo = 0, k_hi = -1, ha = INT_MAX, hb = INT_MIN;
+  if (ea <= eb) {
+    k_lo = max(ea - R, 0) >> 4;
+    k_hi = min(eb + R, W - 1) >> 4;
+    ha = 16 * k_lo;
+    hb = 16 * k_hi + 15;
+  }
+  if (tid == 0) p.band_ext[env * nb + band] = make_int2(ha, hb);
+  const int row = tid & (BH - 1);
+  const int k = tid >> 4;
+  const int c0 = 16 * k;
+  const bool has = k >= k_lo && k <= k_hi;
+  float2 acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
+  if (ea <= eb) {
+    // V covers every in-frame column an H window of [ha, hb] reads (columns
+    // with no non-zero input within R come out as exact zeros)
+    const int c_lo = max(ha - R4, 0);
+    const int c_hi = min(hb + R4, W - 1);
+    const int np = (c_hi - c_lo) / 2 + 1;
+    const bool fast = c0 - R4 >= 0 && c0 + 15 + R4 <= W - 1;
+    for (int l = 0; l < p.n_levels; ++l) {
+      const int RL = p.radius[l];
+      if (RL == 0) {  // identity level (k == 1): straight from the input
+        if (has) {
+          const float w = p.wh[l][0];
+          const float* in = inb + (row + R) * ip + c0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            acc[i] = ffma2(make_float2(w, w), make_float2(in[2 * i], in[2 * i + 1]), acc[i]);
+        }
+        continue;
+      }
+      // V: one (column pair, 8-row half) item per thread
+      if (tid < 2 * np) {
+        const int hf = tid >= np ? 1 : 0;
+        const int c = c_lo + 2 * (tid - hf * np);
+        const float* s = inb + (8 * hf + R - RL) * ip + c;
+        float* dst = vb + 8 * hf * vp + (c - vbase);
+        const bool st_y = c + 1 <= W - 1;
+        switch (RL) {
+#define X(r)                                            \
+  case r:                                               \
+    v5item<r>(p.wv2[l], s, ip, dst, vp, st_y);          \
+    break;
+          TAC5_RADIUS_CASES(X)
+#undef X
+          default:
+            break;
+        }
+      }
+      __syncthreads();
+      if (has) {
+        const float* vrow = vb + row * vp;
+        switch (RL) {
+#define X(r)                                                                   \
+  case r:                                                                      \
+    if (fast)                                                                  \
+      h5fast<r>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc);         \
+    else                                                                       \
+      h5edge<r>(p.wh2[l], vrow - vbase, c0, W, acc);                           \
+    break;
+          TAC5_RADIUS_CASES(X)
+#undef X
+          default:
+            break;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- blurred band out (exact zeros outside [ha, hb]) --------------------------
+  const int y = y0 + row;
+  if (k < nch && y < H) {
+    float4* d = reinterpret_cast<float4*>(p.scratch + env * HW + (long long)y * W + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x, acc[2 * i + 1].y);
+  }
+
+  // ---- contact partials of the band (reduced per env by env_epilogue_kernel) ------
+  if (p.finalize == 0) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    red.swx = fma((double)colsum[q], (double)(4 * cg + q) + 0.5 - (double)p.half_w, red.swx);
+  block_reduce(red, s_red, tid, blockDim.x * blockDim.y);
+  if (tid == 0) {
+    double* q = p.partials + (env * nb + band) * kSumFields;
+    q[0] = red.cnt;
+    q[1] = red.sw;
+    q[2] = red.swx;
+    q[3] = red.swy;
+    q[4] = red.mx;
+    q[5] = red.nf;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernel (b): 4 pixels per thread.  grid (row groups, envs); block (W/4, rpc).
+__global__ void __launch_bounds__(K2T, 4) band_shade_kernel(const __grid_constant__ FrameParams p) {
+  const int W = p.W, H = p.H;
+  const long long env = blockIdx.y;
+  const int gi = threadIdx.x;
+  const int ng = blockDim.x;  // 4-pixel groups per row
+  const int y = blockIdx.x * blockDim.y + threadIdx.y;
+  const int xg = 4 * gi;
+  const long long HW = (long long)H * W;
+  const int lane = (threadIdx.y * ng + gi) & 31;
+  const bool act = y < H;
+  const int yc = act ? y : H - 1;
+  const float* bl = p.scratch + env * HW;
+  uint8_t* out = p.rgb + env * HW * 3;
+
+  // columns whose gradient can be non-zero: band extents of rows y-1..y+1, +-1
+  const int2* ext = p.band_ext + env * p.bands;
+  const int2 e0 = __ldg(ext + (max(yc - 1, 0) >> 4));
+  const int2 e1 = __ldg(ext + (yc >> 4));
+  const int2 e2 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
+  const int sa = min(min(e0.x, e1.x), e2.x);
+  const int sb = max(max(e0.y, e1.y), e2.y);
+  const bool shade = act && sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1;
+  // rows y-1, y, y+1 (float4); every lane takes part in the shuffles
+  const float* rc = bl + (long long)yc * W + xg;
+  float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
+  if (shade) {
+    cc = *reinterpret_cast<const float4*>(rc);
+    mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
+    nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
+  }
+  float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
+  float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
+  if (shade) {
+    if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
+    if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
+    const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
+    const float m[4] = {mm.x, mm.y, mm.z, mm.w};
+    const float n[4] = {nn.x, nn.y, nn.z, nn.w};
+    const bool top = (yc == 0), bot = (yc == H - 1);
+    const float sy = (top || bot) ? p.inv_p : p.inv_2p;
+    float gxs[4], gys[4];
+    if (!top && !bot && xg > 0 && xg + 4 < W) {  // interior: central differences
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        gxs[k] = (c[k + 2] - c[k]) * p.inv_2p;
+        gys[k] = (n[k] - m[k]) * p.inv_2p;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int x = xg + k;
+        const bool lft = (x == 0), rgt = (x == W - 1);
+        const float xr = rgt ? c[k + 1] : c[k + 2];
+        const float xl = lft ? c[k + 1] : c[k];
+        gxs[k] = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
+        const float yb = bot ? c[k + 1] : n[k];
+        const float yt = top ? c[k + 1] : m[k];
+        gys[k] = (yb - yt) * sy;
+      }
+    }
+    const float* bgp = p.bg + ((long long)yc * W + xg) * 3;
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);
+    const float4 b2 = __ldg(reinterpret_cast<const float4*>(bgp) + 2);
+    const float bgv[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+    float sf[4] = {1.f, 1.f, 1.f, 1.f};
+    if (p.shadow) {
+      const float4 f4 = __ldg(reinterpret_cast<const float4*>(p.shadow + env * HW + (long long)yc * W + xg));
+      sf[0] = f4.x; sf[1] = f4.y; sf[2] = f4.z; sf[3] = f4.w;
+    }
+    uint32_t qb[12];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
+      const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
+      const float4 a0 = __ldg(a0p.lut), c0 = __ldg(a0p.lut + 1), d0 = __ldg(a0p.lut + 2), e0 = __ldg(a0p.lut + 3);
+      const float4 a1 = __ldg(a1p.lut), c1 = __ldg(a1p.lut + 1), d1 = __ldg(a1p.lut + 2), e1 = __ldg(a1p.lut + 3);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const Px& pp = s ? a1p : a0p;
+        float r = bgv[6 * h + 3 * s], g = bgv[6 * h + 3 * s + 1], b = bgv[6 * h + 3 * s + 2];
+        if (s)
+          add_lut(a1, c1, d1, e1, pp.nx, pp.ny, r, g, b);
+        else
+          add_lut(a0, c0, d0, e0, pp.nx, pp.ny, r, g, b);
+        if (p.shadow) {  // clip, then the multiplicative shadow (REF/optical.py:246, :299)
+          const float f = sf[2 * h + s];
+          r = clampf(r, 0.f, 255.f) * f;
+          g = clampf(g, 0.f, 255.f) * f;
+          b = clampf(b, 0.f, 255.f) * f;
+        }
+        qb[6 * h + 3 * s] = u8sat(r);
+        qb[6 * h + 3 * s + 1] = u8sat(g);
+        qb[6 * h + 3 * s + 2] = u8sat(b);
+      }
+    }
+    uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)yc * W + xg) * 3);
+    d[0] = qb[0] | (qb[1] << 8) | (qb[2] << 16) | (qb[3] << 24);
+    d[1] = qb[4] | (qb[5] << 8) | (qb[6] << 16) | (qb[7] << 24);
+    d[2] = qb[8] | (qb[9] << 8) | (qb[10] << 16) | (qb[11] << 24);
+  } else if (act) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(p.bg_u8 + ((long long)yc * W + xg) * 3);
+    uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)yc * W + xg) * 3);
+    d[0] = __ldg(s);
+    d[1] = __ldg(s + 1);
+    d[2] = __ldg(s + 2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernel (c): per-env epilogue after every band is blurred and shaded.  The
+// band partials are reduced in a fixed order (deterministic), then contact /
+// summary / load (REF/marker.py:103-140), displacements (REF/marker.py:143-165)
+// and the dot splat (REF/marker.py:203-234).  One 128-thread CTA per env.
+__global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant__ FrameParams p) {
+  __shared__ double s_dbl[8];
+  __shared__ int s_int[2 * 1024];
+  const long long env = blockIdx.x;
+  const int nb = p.bands;
+  if (threadIdx.x == 0) {
+    double cnt = 0, sw = 0, swx = 0, swy = 0, nf = 0;
+    float mx = 0.f;
+    const double* q = p.partials + env * nb * kSumFields;
+    for (int s = 0; s < nb; ++s) {
+      cnt += q[s * 8 + 0];
+      sw += q[s * 8 + 1];
+      swx += q[s * 8 + 2];
+      swy += q[s * 8 + 3];
+      mx = fmaxf(mx, (float)q[s * 8 + 4]);
+      nf += q[s * 8 + 5];
+    }
+    finalize_load(p, env, cnt, sw, swx, swy, mx, nf, s_dbl);
+  }
+  __syncthreads();
+  if (p.finalize != 2) return;
+  const Load l = load_from(s_dbl);
+  const int nm = p.mg.rows * p.mg.cols;
+  markers_block(p.mg, l, p.disp ? p.disp + env * (long long)nm * 2 : nullptr,
+                p.splat ? p.rgb + env * (long long)p.H * p.W * 3 : nullptr, nullptr, s_int, s_int + nm);
+}
+
+size_t band_blur_smem_bytes(const FrameParams& p) {
+  return sizeof(float) * ((size_t)(BH + 2 * p.R) * p.in_pitch + (size_t)BH * p.v_pitch);
+}
+
+bool frame5_eligible(const FrameParams& p) {
+  if (p.strips != 1 || p.W % 16 != 0 || p.W > 320 || p.W < 16) return false;
+  if (p.R < 1 || p.R > 16) return false;
+  if (p.mg.rows * p.mg.cols > 1024) return false;
+  const int ng = p.W / 4;
+  if ((ng * (K1T / ng)) % 32 != 0) return false;  // whole warps (shuffles, block_reduce)
+  return band_blur_smem_bytes(p) <= 227 * 1024;
+}
+
+cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s) {
+  const size_t smem = band_blur_smem_bytes(p0);
+  cudaError_t e = cudaFuncSetAttribute(band_blur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (p0.n_env == 0) return cudaSuccess;
+  const long long HW = (long long)p0.H * p0.W;
+  const int ng = p0.W / 4;
+  const dim3 b1(ng, K1T / ng);
+  const int rpc = K2T / ng;
+  const dim3 b2(ng, rpc);
+  const unsigned nq = (unsigned)((p0.H + rpc - 1) / rpc);
+  const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
+  for (long long e0 = 0; e0 < p0.n_env; e0 += chunk) {
+    const long long n = std::min(chunk, p0.n_env - e0);
+    FrameParams p = p0;
+    // per-chunk views (every per-env pointer advanced by e0 envs)
+    p.in = p0.in + e0 * HW;
+    p.rgb = p0.rgb + e0 * HW * 3;
+    p.scratch = p0.blurred ? p0.blurred + e0 * HW : p0.scratch;
+    p.partials = p0.partials + e0 * p0.bands * kSumFields;
+    if (p0.shadow) p.shadow = p0.shadow + e0 * HW;
+    p.n_env = n;
+    band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (p0.finalize != 0) {
+    env_epilogue_kernel<<<(unsigned)p0.n_env, 128, 0, s>>>(p0);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace tac

@@ -55,6 +55,8 @@ struct FrameParams {
   int radius[TAC_MAX_LEVELS];
   float wv[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // vertical taps, centre first
   float wh[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // horizontal taps, folded with 1/L
+  float2 wv2[TAC_MAX_LEVELS][17];                // (w, w) pairs of wv / wh for FFMA2 (radius <= 16)
+  float2 wh2[TAC_MAX_LEVELS][17];
   // clamp / contact
   float rest;            // gel thickness rounded to fp32
   float rest_lo;         // rest - (double)rest: the clamp runs in ~fp64 accuracy
@@ -90,6 +92,13 @@ struct FrameParams {
   float* disp;           // nullable
   int splat;
   const float* shadow;   // nullable [N][H][W] multiplicative shadow factor
+  long long* prof;       // nullable diagnostics: [prof_envs][nblocks][8] clock64 stamps
+  long long prof_envs;
+  // band-tiled two-kernel path (tac_frame5.cu)
+  int bands;             // ceil(H / 16)
+  long long chunk;       // envs per (blur, shade) launch pair
+  int2* band_ext;        // workspace [chunk][bands] blurred non-zero column range
+  float* scratch;        // workspace [chunk][H][W] blurred (or the caller's blurred output)
 };
 
 // add_shadows march tables (REF/optical.py:283-299), built on the host.
@@ -108,6 +117,13 @@ cudaError_t launch_shadow(const ShadowParams& s, const float* in, int input_dept
 
 size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
+// slot-ring fused kernel (tac_frame4.cu): R <= RB, TMA-aligned input
+size_t frame4_smem_bytes(const FrameParams& p);
+bool frame4_eligible(const FrameParams& p);
+cudaError_t launch_frame4(const FrameParams& p, cudaStream_t s);
+// band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
+bool frame5_eligible(const FrameParams& p);
+cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,
                                cudaStream_t s);
 cudaError_t launch_normals(const float* elev, float* normals, int H, int W, float inv_p,

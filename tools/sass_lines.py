@@ -41,7 +41,8 @@ for f in os.listdir(tmp):
             lines_of[int(m.group(1), 16)] = (cur_line, m.group(2))
     break
 
-exp = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+exp = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                      "-k", "regex:" + os.environ.get("KFILTER", max(re.findall(r"[a-z_]+", kern), key=len))],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(exp)))
 hdr = rows[1]
