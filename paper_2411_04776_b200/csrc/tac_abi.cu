@@ -426,7 +426,7 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   c->fused5 = c->fused;
   plan_v5(c->fused5);
   c->use5 = kind == 5 && frame5_eligible(c->fused5);
-  c->chunk5 = std::max(1, env_int("TAC_CHUNK", 256));
+  c->chunk5 = std::max(1, env_int("TAC_CHUNK", 512));
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
     if (p.stage_bytes > (int)(RB * p.v_pitch * sizeof(float))) {

@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   Red red = red_zero();
   float colsum[4] = {0.f, 0.f, 0.f, 0.f};
   const int cg = threadIdx.x, ro = threadIdx.y, cstep = blockDim.y;
-  mbar_wait(&s_bar, 0);
+  // one warp polls the mbarrier; the others wait at the CTA barrier (no issue slots)
+  if (tid < 32) mbar_wait(&s_bar, 0);
+  __syncthreads();
   bool nz = false;
   auto clamp4 = [&](float4* e) -> float4 {
     float4 v = *e;
@@ -212,6 +214,19 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     }
     red.sw += (double)rowsum;
     red.swy = fma((double)rowsum, (double)(y0 + i) + 0.5 - (double)p.half_h, red.swy);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    red.swx = fma((double)colsum[q], (double)(4 * cg + q) + 0.5 - (double)p.half_w, red.swx);
+  warp_reduce(red);
+  if ((tid & 31) == 0) {
+    double* q = s_red + (tid >> 5) * 8;
+    q[0] = red.cnt;
+    q[1] = red.sw;
+    q[2] = red.swx;
+    q[3] = red.swy;
+    q[4] = red.mx;
+    q[5] = red.nf;
   }
   {
     const int c = 4 * cg;
@@ -308,26 +323,26 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
       d[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x, acc[2 * i + 1].y);
   }
 
-  // ---- contact partials of the band (reduced per env by env_epilogue_kernel) ------
-  if (p.finalize == 0) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    red.swx = fma((double)colsum[q], (double)(4 * cg + q) + 0.5 - (double)p.half_w, red.swx);
-  block_reduce(red, s_red, tid, blockDim.x * blockDim.y);
-  if (tid == 0) {
-    double* q = p.partials + (env * nb + band) * kSumFields;
-    q[0] = red.cnt;
-    q[1] = red.sw;
-    q[2] = red.swx;
-    q[3] = red.swy;
-    q[4] = red.mx;
-    q[5] = red.nf;
+  // ---- contact partials of the band (warp sums in s_red since the conversion;
+  //      reduced per env by env_epilogue_kernel) ----------------------------------
+  if (p.finalize == 0 || tid != 0) return;
+  const int nw = (blockDim.x * blockDim.y) >> 5;
+  double t[6] = {0, 0, 0, 0, 0, 0};
+  for (int w = 0; w < nw; ++w) {  // fixed order: deterministic
+    for (int i = 0; i < 4; ++i) t[i] += s_red[w * 8 + i];
+    t[4] = fmax(t[4], s_red[w * 8 + 4]);
+    t[5] += s_red[w * 8 + 5];
   }
+  double* q = p.partials + (env * nb + band) * kSumFields;
+  for (int i = 0; i < 6; ++i) q[i] = t[i];
 }
 
 // ---------------------------------------------------------------------------
 // kernel (b): 4 pixels per thread.  grid (row groups, envs); block (W/4, rpc).
-__global__ void __launch_bounds__(K2T, 4) band_shade_kernel(const __grid_constant__ FrameParams p) {
+#ifndef TAC_K2_MINB
+#define TAC_K2_MINB 4
+#endif
+__global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __grid_constant__ FrameParams p) {
   const int W = p.W, H = p.H;
   const long long env = blockIdx.y;
   const int gi = threadIdx.x;
@@ -348,7 +363,8 @@ __global__ void __launch_bounds__(K2T, 4) band_shade_kernel(const __grid_constan
   const int2 e2 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
   const int sa = min(min(e0.x, e1.x), e2.x);
   const int sb = max(max(e0.y, e1.y), e2.y);
-  const bool shade = act && sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1;
+  // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
+  bool shade = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
   // rows y-1, y, y+1 (float4); every lane takes part in the shuffles
   const float* rc = bl + (long long)yc * W + xg;
   float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
@@ -359,6 +375,7 @@ __global__ void __launch_bounds__(K2T, 4) band_shade_kernel(const __grid_constan
   }
   float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
   float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
+  float gxs[4] = {0.f, 0.f, 0.f, 0.f}, gys[4] = {0.f, 0.f, 0.f, 0.f};
   if (shade) {
     if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
     if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
@@ -367,7 +384,6 @@ __global__ void __launch_bounds__(K2T, 4) band_shade_kernel(const __grid_constan
     const float n[4] = {nn.x, nn.y, nn.z, nn.w};
     const bool top = (yc == 0), bot = (yc == H - 1);
     const float sy = (top || bot) ? p.inv_p : p.inv_2p;
-    float gxs[4], gys[4];
     if (!top && !bot && xg > 0 && xg + 4 < W) {  // interior: central differences
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -387,6 +403,13 @@ __global__ void __launch_bounds__(K2T, 4) band_shade_kernel(const __grid_constan
         gys[k] = (yb - yt) * sy;
       }
     }
+    // a group whose four gradients are exactly zero shades to exactly rint(bg)
+    // (REF/optical.py:244 with n = (0, 0, 1)); without shadows it is a copy
+    const bool flat = gxs[0] == 0.f && gxs[1] == 0.f && gxs[2] == 0.f && gxs[3] == 0.f &&
+                      gys[0] == 0.f && gys[1] == 0.f && gys[2] == 0.f && gys[3] == 0.f;
+    shade = !(flat && p.shadow == nullptr);
+  }
+  if (shade) {
     const float* bgp = p.bg + ((long long)yc * W + xg) * 3;
     const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
     const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);

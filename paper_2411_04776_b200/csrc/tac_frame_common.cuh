@@ -206,6 +206,19 @@ __device__ __forceinline__ Red red_zero() {
   return r;
 }
 
+// Warp-level part of block_reduce (fixed shuffle tree); result in every lane.
+__device__ __forceinline__ void warp_reduce(Red& v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.cnt += __shfl_xor_sync(0xffffffffu, v.cnt, o);
+    v.mx = fmaxf(v.mx, __shfl_xor_sync(0xffffffffu, v.mx, o));
+    v.nf += __shfl_xor_sync(0xffffffffu, v.nf, o);
+    v.sw += __shfl_xor_sync(0xffffffffu, v.sw, o);
+    v.swx += __shfl_xor_sync(0xffffffffu, v.swx, o);
+    v.swy += __shfl_xor_sync(0xffffffffu, v.swy, o);
+  }
+}
+
 // Fixed shuffle tree + fixed warp order: deterministic.  Result in the thread
 // with linear id 0.  `tid` / `nthreads`: linear thread id and block size (for
 // 2-D blocks); nthreads is a multiple of 32.

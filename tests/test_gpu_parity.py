@@ -440,28 +440,35 @@ class TestShadows:
 
 
 class TestKernelVariants:
-    """The slot-ring kernel (tac_frame4.cu, default for R <= 16 with aligned
-    rows) against the strip-streaming kernel (tac_frame.cu, TAC_FRAME=3) on a
-    full-size configs[2] batch: same arithmetic up to the fp32 summation order
-    of the levels, so RGB may differ by a rounding flip, blur by ulps."""
+    """The band-tiled two-kernel path (tac_frame5.cu, default: TAC_FRAME=5) and
+    the slot-ring fused kernel (tac_frame4.cu, TAC_FRAME=4) against the
+    strip-streaming fused kernel (tac_frame.cu, TAC_FRAME=3) on a full-size
+    configs[2] batch: the same arithmetic up to the fp32 summation order of the
+    levels, so RGB may differ by a rounding flip and the blur by ulps; the
+    exact-zero skips must agree exactly."""
 
+    @pytest.mark.parametrize("variant", ["4", "5"])
     @pytest.mark.parametrize("kind", [None, "sphere", "perlin"])
-    def test_slot_ring_matches_strip_kernel(self, monkeypatch, kind):
+    def test_variant_matches_strip_kernel(self, monkeypatch, kind, variant):
         cfg, _ = synthetic.baseline_config(2, 0)
         n = 48
         p = synthetic.indenters(n, 240, 320, 5, fixed_kind=kind)
         depth = synthetic.height_maps(p, 240, 320, dtype=torch.float64).float()
         shear, twist = synthetic.loads(n, 6)
+        monkeypatch.setenv("TAC_FRAME", variant)
         obs4 = run_pipeline(cfg, depth, shear, twist)
         monkeypatch.setenv("TAC_FRAME", "3")
-        obs3 = run_pipeline(cfg, depth, shear, twist)
+        cfg3, _ = synthetic.baseline_config(2, 0)  # a new config object -> a new context
+        obs3 = run_pipeline(cfg3, depth, shear, twist)
         d = (obs4.rgb.int() - obs3.rgb.int()).abs()
-        assert int(d.max()) <= 1
+        # a ulp of blur can flip a LUT bin near a boundary (then |d| > 1 is possible)
+        assert float((d <= 1).float().mean()) >= 0.99999
         assert float((d == 0).float().mean()) >= 0.9999
         b4, b3 = obs4.blurred.cpu().numpy(), obs3.blurred.cpu().numpy()
         assert normwise(b4, b3) <= 1e-6
         assert np.array_equal(b4 == 0, b3 == 0)  # the exact-zero skip is exact
-        assert normwise(obs4.disp.cpu().numpy(), obs3.disp.cpu().numpy()) <= 1e-6
+        # contact sums are accumulated in a different (fixed) order per variant
+        assert normwise(obs4.disp.cpu().numpy(), obs3.disp.cpu().numpy()) <= 1e-5
         s4, s3 = obs4.summary.cpu().numpy(), obs3.summary.cpu().numpy()
         assert np.array_equal(s4[:, 0], s3[:, 0]) and np.array_equal(s4[:, 1], s3[:, 1])
         assert np.allclose(s4, s3, rtol=1e-5, atol=1e-9)
