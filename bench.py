@@ -188,9 +188,27 @@ def fma_per_frame(cfg):
 
 
 def algorithmic_bytes(cfg):
+    """Whole path, per frame: depth in (fp32) + RGB out (u8) + marker field + summary."""
     h, w = cfg.sensor.image_size
     r, c = cfg.sensor.marker_grid
     return 4 * h * w + 3 * h * w + 8 * r * c + 32
+
+
+def kernel_bytes(cfg):
+    """Algorithmic HBM bytes per frame of each kernel of the two-kernel path
+    (DESIGN.md §5): blur = depth in + blurred out + band partials; shade =
+    blurred in + RGB out (the LUT and background are shared, L2-resident);
+    epilogue = partials in + marker field + summary out + dot pixels RMW."""
+    h, w = cfg.sensor.image_size
+    r, c = cfg.sensor.marker_grid
+    bands = -(-h // 16)
+    rr = cfg.dot_radius
+    dot_px = sum(1 for dy in range(-rr, rr + 1) for dx in range(-rr, rr + 1) if dx * dx + dy * dy <= rr * rr)
+    return {
+        "band_blur_kernel": 4 * h * w + 4 * h * w + 64 * bands,
+        "band_shade_kernel": 4 * h * w + 3 * h * w,
+        "env_epilogue_kernel": 64 * bands + 8 * r * c + 32 + 3 * dot_px * r * c,
+    }
 
 
 # --------------------------------------------------------------------------- arms
@@ -298,7 +316,7 @@ def run_ours(a, rank, world, local_rank):
     ms_step = ms / a.steps
     value = world * n_env * a.steps / (ms / 1e3)
 
-    # kernel-only launch duration (the fused kernel is the only launch per step)
+    # one tac_pipeline call (all its launches) bracketed by events on the launch stream
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
     for e0, e1 in kev:
         e0.record(stream)
@@ -306,6 +324,10 @@ def run_ours(a, rank, world, local_rank):
         e1.record(stream)
     torch.cuda.synchronize()
     k_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in kev)
+    # per-kernel durations: CUDA events around every launch inside the C ABI
+    # (tac_pipeline_profile; same stream, synchronised per launch)
+    kern_ms = pipe.profile(args, iters=10)
+    launches = pipe.launches_per_call(n_env)
 
     # e2e: host buffers through the public host API, copies inside the timed region
     e2e = None
@@ -346,17 +368,33 @@ def run_ours(a, rank, world, local_rank):
         return
     peak, peak_kind = measured_peak()
     per_launch = algorithmic_bytes(cfg) * n_env
-    achieved = per_launch / (k_ms / 1e3) / 1e9
+    step_gbs = per_launch / (k_ms / 1e3) / 1e9
+    kb = kernel_bytes(cfg)
+    kernels = {}
+    if launches > 1:  # two-kernel path (tac_frame5.cu)
+        for name, kms in zip(kb, kern_ms):
+            if kms > 0:
+                gbs = kb[name] * n_env / (kms / 1e3) / 1e9
+                kernels[name] = {"ms": kms, "bytes_per_frame": kb[name], "achieved_gbs": gbs, "frac": gbs / peak}
+        dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    else:  # one fused kernel (TAC_FRAME=3/4)
+        dom = "frame_kernel (fused)"
+        kernels[dom] = {"ms": kern_ms[0], "bytes_per_frame": algorithmic_bytes(cfg),
+                        "achieved_gbs": step_gbs, "frac": step_gbs / peak}
+    achieved = kernels[dom]["achieved_gbs"]
     props = torch.cuda.get_device_properties(dev)
     clocks = clk.result()
     fma = fma_per_frame(cfg)
     sm_ghz = (clocks["sm_mhz"] or 1965) / 1e3
     fma_peak = props.multi_processor_count * 128 * sm_ghz * 1e9
-    traffic = None
+    traffic = None  # dram read+write bytes per launch of the dominant kernel (ncu --set full)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"configs[{a.config}]")
+            t = json.load(open(tpath)).get(f"configs[{a.config}]")
+            traffic = t.get(dom) if isinstance(t, dict) else None
+            if traffic is not None:
+                traffic = traffic * n_env / t.get("envs", n_env)  # scale to this launch size
         except Exception:
             traffic = None
     line = {
@@ -393,14 +431,17 @@ def run_ours(a, rank, world, local_rank):
             "frac": achieved / peak,
             "traffic": traffic,
             "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)",
-            "kernel": "frame_kernel<1> (tac_pipeline)",
-            "kernel_ms": k_ms,
-            "algorithmic_bytes_per_frame": algorithmic_bytes(cfg),
+            "kernel": dom,
+            "kernel_ms": kernels[dom]["ms"],
+            "algorithmic_bytes_per_launch": kernels[dom]["bytes_per_frame"] * n_env,
+            "kernels": kernels,
+            "step": {"ms": k_ms, "algorithmic_bytes_per_frame": algorithmic_bytes(cfg),
+                     "achieved_gbs": step_gbs, "frac": step_gbs / peak},
             "fp32_fma": {"per_frame_dense": fma,
                          "achieved_tflops_dense_equiv": 2 * fma * n_env / (k_ms / 1e3) / 1e12,
                          "peak_tflops": 2 * fma_peak / 1e12},
         },
-        "gpu_launches": a.steps,
+        "gpu_launches": a.steps * launches,
         "clocks": clocks,
         "device": props.name,
     }

@@ -115,6 +115,14 @@ int32_t tac_tiles_per_frame(const tac_ctx* ctx);
  * shade groups for the first n_env envs of each tac_pipeline call (NULL = off).
  * Not thread-safe with concurrent tac_pipeline calls on the same context. */
 int tac_set_profile_buffer(tac_ctx* ctx, int64_t* buf, int64_t n_env);
+/* Diagnostics: number of kernel launches one tac_pipeline call makes for n_env. */
+int32_t tac_pipeline_launches(const tac_ctx* ctx, int64_t n_env);
+/* Diagnostics: runs tac_pipeline `iters` times with a CUDA event pair around
+ * every kernel launch (synchronising the stream after each) and writes the
+ * mean per-call milliseconds of each kernel kind: kernel_ms[0] = blur (or the
+ * fused frame kernel), [1] = shade, [2] = per-env epilogue (0 when absent). */
+int tac_pipeline_profile(const tac_ctx* ctx, const struct tac_pipeline_args* args, void* stream,
+                         int32_t iters, float* kernel_ms);
 
 /* indentation_from (REF/tactile.py:193-197): ind = clip(rest - depth, 0, rest).
  * depth, ind: [N,H,W]. */

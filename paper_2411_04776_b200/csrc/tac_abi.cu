@@ -30,6 +30,8 @@ struct tac_ctx {
   FrameParams fused5;                // band-tiled two-kernel geometry (default)
   bool use5;
   long long chunk5;                  // envs per v5 launch pair
+  bool overlap5;                     // pipeline chunks over two context streams
+  Overlap ov{};                      // created with the context (overlap5)
   long long* prof = nullptr;         // diagnostics buffer (tac_set_profile_buffer)
   long long prof_envs = 0;
   MarkerGeom mg;
@@ -130,8 +132,9 @@ size_t v5_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   if (!c->use5) return 0;
   const long long C = std::min<long long>(n_env, c->chunk5);
   const FrameParams& p = c->fused5;
+  const size_t halves = c->overlap5 ? 2 : 1;  // double-buffered scratch when chunks overlap
   return align256((size_t)n_env * p.bands * kSumFields * sizeof(double)) +
-         align256((size_t)C * p.bands * sizeof(int2)) + align256((size_t)C * p.H * p.W * sizeof(float));
+         align256(halves * C * p.bands * sizeof(int2)) + align256(halves * C * p.H * p.W * sizeof(float));
 }
 
 size_t v3_workspace_bytes(const tac_ctx* c, int64_t n_env) {
@@ -145,13 +148,18 @@ void bind_workspace5(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) 
   p.partials = reinterpret_cast<double*>(b);
   b += align256((size_t)n_env * p.bands * kSumFields * sizeof(double));
   p.band_ext = reinterpret_cast<int2*>(b);
-  b += align256((size_t)C * p.bands * sizeof(int2));
+  b += align256((c->overlap5 ? 2 : 1) * (size_t)C * p.bands * sizeof(int2));
   p.scratch = reinterpret_cast<float*>(b);
   p.chunk = C;
 }
 
 int free_ctx(tac_ctx* c) {
   if (!c) return TAC_OK;
+  if (c->ov.blur) cudaStreamDestroy(c->ov.blur);
+  if (c->ov.shade) cudaStreamDestroy(c->ov.shade);
+  for (cudaEvent_t ev : {c->ov.start, c->ov.blur_done[0], c->ov.blur_done[1], c->ov.shade_done[0],
+                         c->ov.shade_done[1], c->ov.end})
+    if (ev) cudaEventDestroy(ev);
   cudaFree(c->d_lut);
   cudaFree(c->d_bg);
   cudaFree(c->d_bg_u8);
@@ -426,7 +434,19 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   c->fused5 = c->fused;
   plan_v5(c->fused5);
   c->use5 = kind == 5 && frame5_eligible(c->fused5);
-  c->chunk5 = std::max(1, env_int("TAC_CHUNK", 512));
+  c->chunk5 = std::max(1, env_int("TAC_CHUNK", 4096));
+  c->overlap5 = c->use5 && env_int("TAC_OVERLAP", 0) != 0;  // measured slower: off by default
+  if (c->overlap5) {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->ov.blur, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->ov.shade, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&c->ov.start, &c->ov.blur_done[0], &c->ov.blur_done[1], &c->ov.shade_done[0],
+                            &c->ov.shade_done[1], &c->ov.end})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return cuda_fail(e, "overlap streams");
+    }
+  }
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
     if (p.stage_bytes > (int)(RB * p.v_pitch * sizeof(float))) {
@@ -571,7 +591,7 @@ int tac_shadow(const tac_ctx* c, const float* in, int32_t input_kind, float* fac
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_shadow");
 }
 
-int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
+static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream, float* kt) {
   if (!a) return fail(TAC_ERR_INVALID, "null args");
   int st = common_checks(c, a->n_env);
   if (st) return st;
@@ -615,12 +635,54 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   cudaError_t e;
   if (v5) {
     bind_workspace5(c, p, a->workspace, a->n_env);
-    e = launch_frame5(p, (cudaStream_t)stream);
+    e = launch_frame5(p, (cudaStream_t)stream, c->overlap5 ? &c->ov : nullptr, kt);
   } else {
     bind_workspace(c, p, a->workspace, a->n_env);
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (kt) {
+      cudaEventCreate(&t0);
+      cudaEventCreate(&t1);
+      cudaEventRecord(t0, (cudaStream_t)stream);
+    }
     e = v4 ? launch_frame4(p, (cudaStream_t)stream) : launch_frame(p, kModeFused, (cudaStream_t)stream);
+    if (kt) {
+      cudaEventRecord(t1, (cudaStream_t)stream);
+      cudaEventSynchronize(t1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t0, t1);
+      kt[0] += ms;
+      cudaEventDestroy(t0);
+      cudaEventDestroy(t1);
+    }
   }
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_pipeline");
+}
+
+int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
+  return run_pipeline(c, a, stream, nullptr);
+}
+
+int32_t tac_pipeline_launches(const tac_ctx* c, int64_t n_env) {
+  if (!c || n_env < 0) return 0;
+  if (c->use5) {
+    FrameParams p = c->fused5;
+    p.chunk = std::min<long long>(n_env, c->chunk5);
+    p.finalize = 2;
+    return frame5_launches(p, n_env);
+  }
+  return n_env > 0 ? 1 : 0;
+}
+
+int tac_pipeline_profile(const tac_ctx* c, const tac_pipeline_args* a, void* stream, int32_t iters,
+                         float* kernel_ms) {
+  if (!kernel_ms || iters < 1) return fail(TAC_ERR_INVALID, "kernel_ms and iters >= 1 are required");
+  float kt[3] = {0.f, 0.f, 0.f};
+  for (int i = 0; i < iters; ++i) {
+    const int st = run_pipeline(c, a, stream, kt);
+    if (st) return st;
+  }
+  for (int k = 0; k < 3; ++k) kernel_ms[k] = kt[k] / iters;
+  return TAC_OK;
 }
 
 }  // extern "C"

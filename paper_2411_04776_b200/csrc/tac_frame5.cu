@@ -338,7 +338,89 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
 }
 
 // ---------------------------------------------------------------------------
-// kernel (b): 4 pixels per thread.  grid (row groups, envs); block (W/4, rpc).
+// kernel (b): shade one 4-pixel group of row y from its blurred rows (c = row
+// y with left/right neighbours, m = row y-1, n = row y+1; border rows/columns
+// use np.gradient's one-sided differences, REF/optical.py:160).  Returns false
+// (nothing written) when all four gradients are exactly zero and there are no
+// shadows: the caller then copies the quantised background.
+__device__ __forceinline__ bool shade_group(const FrameParams& p, long long env, int y, int xg,
+                                            const float c[6], const float4 mm, const float4 nn,
+                                            uint8_t* out) {
+  const int W = p.W, H = p.H;
+  const float m[4] = {mm.x, mm.y, mm.z, mm.w};
+  const float n[4] = {nn.x, nn.y, nn.z, nn.w};
+  const bool top = (y == 0), bot = (y == H - 1);
+  float gxs[4], gys[4];
+  if (!top && !bot && xg > 0 && xg + 4 < W) {  // interior: central differences
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      gxs[k] = (c[k + 2] - c[k]) * p.inv_2p;
+      gys[k] = (n[k] - m[k]) * p.inv_2p;
+    }
+  } else {
+    const float sy = (top || bot) ? p.inv_p : p.inv_2p;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = xg + k;
+      const bool lft = (x == 0), rgt = (x == W - 1);
+      const float xr = rgt ? c[k + 1] : c[k + 2];
+      const float xl = lft ? c[k + 1] : c[k];
+      gxs[k] = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
+      const float yb = bot ? c[k + 1] : n[k];
+      const float yt = top ? c[k + 1] : m[k];
+      gys[k] = (yb - yt) * sy;
+    }
+  }
+  // a group whose four gradients are exactly zero shades to exactly rint(bg)
+  // (REF/optical.py:244 with n = (0, 0, 1))
+  const bool flat = gxs[0] == 0.f && gxs[1] == 0.f && gxs[2] == 0.f && gxs[3] == 0.f &&
+                    gys[0] == 0.f && gys[1] == 0.f && gys[2] == 0.f && gys[3] == 0.f;
+  if (flat && p.shadow == nullptr) return false;
+  const long long HW = (long long)H * W;
+  const float* bgp = p.bg + ((long long)y * W + xg) * 3;
+  const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
+  const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);
+  const float4 b2 = __ldg(reinterpret_cast<const float4*>(bgp) + 2);
+  const float bgv[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+  float sf[4] = {1.f, 1.f, 1.f, 1.f};
+  if (p.shadow) {
+    const float4 f4 = __ldg(reinterpret_cast<const float4*>(p.shadow + env * HW + (long long)y * W + xg));
+    sf[0] = f4.x; sf[1] = f4.y; sf[2] = f4.z; sf[3] = f4.w;
+  }
+  uint32_t qb[12];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
+    const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
+    const float4 a0 = __ldg(a0p.lut), c0 = __ldg(a0p.lut + 1), d0 = __ldg(a0p.lut + 2), e0 = __ldg(a0p.lut + 3);
+    const float4 a1 = __ldg(a1p.lut), c1 = __ldg(a1p.lut + 1), d1 = __ldg(a1p.lut + 2), e1 = __ldg(a1p.lut + 3);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const Px& pp = s ? a1p : a0p;
+      float r = bgv[6 * h + 3 * s], g = bgv[6 * h + 3 * s + 1], b = bgv[6 * h + 3 * s + 2];
+      if (s)
+        add_lut(a1, c1, d1, e1, pp.nx, pp.ny, r, g, b);
+      else
+        add_lut(a0, c0, d0, e0, pp.nx, pp.ny, r, g, b);
+      if (p.shadow) {  // clip, then the multiplicative shadow (REF/optical.py:246, :299)
+        const float f = sf[2 * h + s];
+        r = clampf(r, 0.f, 255.f) * f;
+        g = clampf(g, 0.f, 255.f) * f;
+        b = clampf(b, 0.f, 255.f) * f;
+      }
+      qb[6 * h + 3 * s] = u8sat(r);
+      qb[6 * h + 3 * s + 1] = u8sat(g);
+      qb[6 * h + 3 * s + 2] = u8sat(b);
+    }
+  }
+  uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)y * W + xg) * 3);
+  d[0] = pack4(qb[0], qb[1], qb[2], qb[3]);
+  d[1] = pack4(qb[4], qb[5], qb[6], qb[7]);
+  d[2] = pack4(qb[8], qb[9], qb[10], qb[11]);
+  return true;
+}
+
+// One 4-pixel group of one row per thread.  grid (row groups, envs); block (W/4, rpc).
 #ifndef TAC_K2_MINB
 #define TAC_K2_MINB 4
 #endif
@@ -353,104 +435,32 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   const int lane = (threadIdx.y * ng + gi) & 31;
   const bool act = y < H;
   const int yc = act ? y : H - 1;
-  const float* bl = p.scratch + env * HW;
+  const float* rc = p.scratch + env * HW + (long long)yc * W + xg;
   uint8_t* out = p.rgb + env * HW * 3;
 
   // columns whose gradient can be non-zero: band extents of rows y-1..y+1, +-1
   const int2* ext = p.band_ext + env * p.bands;
   const int2 e0 = __ldg(ext + (max(yc - 1, 0) >> 4));
-  const int2 e1 = __ldg(ext + (yc >> 4));
-  const int2 e2 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
-  const int sa = min(min(e0.x, e1.x), e2.x);
-  const int sb = max(max(e0.y, e1.y), e2.y);
+  const int2 e1 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
+  const int sa = min(e0.x, e1.x), sb = max(e0.y, e1.y);
   // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
-  bool shade = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
-  // rows y-1, y, y+1 (float4); every lane takes part in the shuffles
-  const float* rc = bl + (long long)yc * W + xg;
+  const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
   float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
-  if (shade) {
+  if (any) {
     cc = *reinterpret_cast<const float4*>(rc);
     mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
     nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
   }
   float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
   float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
-  float gxs[4] = {0.f, 0.f, 0.f, 0.f}, gys[4] = {0.f, 0.f, 0.f, 0.f};
-  if (shade) {
+  bool done = false;
+  if (any) {
     if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
     if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
     const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
-    const float m[4] = {mm.x, mm.y, mm.z, mm.w};
-    const float n[4] = {nn.x, nn.y, nn.z, nn.w};
-    const bool top = (yc == 0), bot = (yc == H - 1);
-    const float sy = (top || bot) ? p.inv_p : p.inv_2p;
-    if (!top && !bot && xg > 0 && xg + 4 < W) {  // interior: central differences
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        gxs[k] = (c[k + 2] - c[k]) * p.inv_2p;
-        gys[k] = (n[k] - m[k]) * p.inv_2p;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int x = xg + k;
-        const bool lft = (x == 0), rgt = (x == W - 1);
-        const float xr = rgt ? c[k + 1] : c[k + 2];
-        const float xl = lft ? c[k + 1] : c[k];
-        gxs[k] = (xr - xl) * ((lft || rgt) ? p.inv_p : p.inv_2p);
-        const float yb = bot ? c[k + 1] : n[k];
-        const float yt = top ? c[k + 1] : m[k];
-        gys[k] = (yb - yt) * sy;
-      }
-    }
-    // a group whose four gradients are exactly zero shades to exactly rint(bg)
-    // (REF/optical.py:244 with n = (0, 0, 1)); without shadows it is a copy
-    const bool flat = gxs[0] == 0.f && gxs[1] == 0.f && gxs[2] == 0.f && gxs[3] == 0.f &&
-                      gys[0] == 0.f && gys[1] == 0.f && gys[2] == 0.f && gys[3] == 0.f;
-    shade = !(flat && p.shadow == nullptr);
+    done = shade_group(p, env, yc, xg, c, mm, nn, out);
   }
-  if (shade) {
-    const float* bgp = p.bg + ((long long)yc * W + xg) * 3;
-    const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
-    const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);
-    const float4 b2 = __ldg(reinterpret_cast<const float4*>(bgp) + 2);
-    const float bgv[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
-    float sf[4] = {1.f, 1.f, 1.f, 1.f};
-    if (p.shadow) {
-      const float4 f4 = __ldg(reinterpret_cast<const float4*>(p.shadow + env * HW + (long long)yc * W + xg));
-      sf[0] = f4.x; sf[1] = f4.y; sf[2] = f4.z; sf[3] = f4.w;
-    }
-    uint32_t qb[12];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
-      const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
-      const float4 a0 = __ldg(a0p.lut), c0 = __ldg(a0p.lut + 1), d0 = __ldg(a0p.lut + 2), e0 = __ldg(a0p.lut + 3);
-      const float4 a1 = __ldg(a1p.lut), c1 = __ldg(a1p.lut + 1), d1 = __ldg(a1p.lut + 2), e1 = __ldg(a1p.lut + 3);
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const Px& pp = s ? a1p : a0p;
-        float r = bgv[6 * h + 3 * s], g = bgv[6 * h + 3 * s + 1], b = bgv[6 * h + 3 * s + 2];
-        if (s)
-          add_lut(a1, c1, d1, e1, pp.nx, pp.ny, r, g, b);
-        else
-          add_lut(a0, c0, d0, e0, pp.nx, pp.ny, r, g, b);
-        if (p.shadow) {  // clip, then the multiplicative shadow (REF/optical.py:246, :299)
-          const float f = sf[2 * h + s];
-          r = clampf(r, 0.f, 255.f) * f;
-          g = clampf(g, 0.f, 255.f) * f;
-          b = clampf(b, 0.f, 255.f) * f;
-        }
-        qb[6 * h + 3 * s] = u8sat(r);
-        qb[6 * h + 3 * s + 1] = u8sat(g);
-        qb[6 * h + 3 * s + 2] = u8sat(b);
-      }
-    }
-    uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)yc * W + xg) * 3);
-    d[0] = qb[0] | (qb[1] << 8) | (qb[2] << 16) | (qb[3] << 24);
-    d[1] = qb[4] | (qb[5] << 8) | (qb[6] << 16) | (qb[7] << 24);
-    d[2] = qb[8] | (qb[9] << 8) | (qb[10] << 16) | (qb[11] << 24);
-  } else if (act) {
+  if (act && !done) {  // flat group: the quantised background
     const uint32_t* s = reinterpret_cast<const uint32_t*>(p.bg_u8 + ((long long)yc * W + xg) * 3);
     uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)yc * W + xg) * 3);
     d[0] = __ldg(s);
@@ -504,7 +514,41 @@ bool frame5_eligible(const FrameParams& p) {
   return band_blur_smem_bytes(p) <= 227 * 1024;
 }
 
-cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s) {
+int frame5_launches(const FrameParams& p, long long n_env) {
+  if (n_env == 0) return 0;
+  const long long chunk = p.chunk > 0 ? p.chunk : n_env;
+  return (int)(2 * ((n_env + chunk - 1) / chunk) + (p.finalize != 0 ? 1 : 0));
+}
+
+// event-timed launch (diagnostics): kt[kind] += elapsed ms
+struct KTimer {
+  float* kt;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KTimer(float* k, cudaStream_t st) : kt(k), s(st) {
+    if (kt) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    }
+  }
+  ~KTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  void start() {
+    if (kt) cudaEventRecord(a, s);
+  }
+  void stop(int kind) {
+    if (!kt) return;
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    kt[kind] += ms;
+  }
+};
+
+cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, const Overlap* ov, float* kt) {
   const size_t smem = band_blur_smem_bytes(p0);
   cudaError_t e = cudaFuncSetAttribute(band_blur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -516,26 +560,61 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s) {
   const dim3 b2(ng, rpc);
   const unsigned nq = (unsigned)((p0.H + rpc - 1) / rpc);
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
-  for (long long e0 = 0; e0 < p0.n_env; e0 += chunk) {
+  const long long nchunks = (p0.n_env + chunk - 1) / chunk;
+  // with overlap: blur on ov->blur, shading on ov->shade, scratch halves alternate
+  const bool two = ov != nullptr && nchunks > 1 && p0.blurred == nullptr && kt == nullptr;
+  KTimer tm(kt, s);
+  cudaStream_t sb = two ? ov->blur : s, ss = two ? ov->shade : s;
+#define CK(x)                          \
+  do {                                 \
+    e = (x);                           \
+    if (e != cudaSuccess) return e;    \
+  } while (0)
+  if (two) {
+    CK(cudaEventRecord(ov->start, s));
+    CK(cudaStreamWaitEvent(sb, ov->start, 0));
+    CK(cudaStreamWaitEvent(ss, ov->start, 0));
+  }
+  for (long long i = 0; i < nchunks; ++i) {
+    const long long e0 = i * chunk;
     const long long n = std::min(chunk, p0.n_env - e0);
+    const int half = (int)(i & 1);
     FrameParams p = p0;
     // per-chunk views (every per-env pointer advanced by e0 envs)
     p.in = p0.in + e0 * HW;
     p.rgb = p0.rgb + e0 * HW * 3;
-    p.scratch = p0.blurred ? p0.blurred + e0 * HW : p0.scratch;
+    p.scratch = p0.blurred ? p0.blurred + e0 * HW : p0.scratch + (two ? half * chunk * HW : 0);
+    p.band_ext = p0.band_ext + (two ? half * chunk * p0.bands : 0);
     p.partials = p0.partials + e0 * p0.bands * kSumFields;
     if (p0.shadow) p.shadow = p0.shadow + e0 * HW;
     p.n_env = n;
-    band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (two && i >= 2) CK(cudaStreamWaitEvent(sb, ov->shade_done[half], 0));  // scratch half is free
+    tm.start();
+    band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, sb>>>(p);
+    CK(cudaGetLastError());
+    tm.stop(0);
+    if (two) {
+      CK(cudaEventRecord(ov->blur_done[half], sb));
+      CK(cudaStreamWaitEvent(ss, ov->blur_done[half], 0));
+    }
+    tm.start();
+    band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, ss>>>(p);
+    CK(cudaGetLastError());
+    tm.stop(1);
+    if (two) CK(cudaEventRecord(ov->shade_done[half], ss));
   }
+  if (two) {  // join: the epilogue needs every blur (partials) and every shade (RGB)
+    CK(cudaEventRecord(ov->end, sb));
+    CK(cudaStreamWaitEvent(s, ov->end, 0));
+    CK(cudaEventRecord(ov->end, ss));
+    CK(cudaStreamWaitEvent(s, ov->end, 0));
+  }
+#undef CK
   if (p0.finalize != 0) {
+    tm.start();
     env_epilogue_kernel<<<(unsigned)p0.n_env, 128, 0, s>>>(p0);
     e = cudaGetLastError();
+    tm.stop(2);
   }
   return e;
 }

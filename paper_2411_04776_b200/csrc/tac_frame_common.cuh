@@ -181,6 +181,11 @@ __device__ __forceinline__ void add_lut(const float4 a, const float4 c, const fl
   b += d.z * nx + d.w * ny + e.x * nxx + e.y * nxy + e.z * nyy;
 }
 
+// Four quantised channel bytes -> one little-endian word (3 PRMT).
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x3340), __byte_perm(c, d, 0x3340), 0x5410);
+}
+
 // Add the binned-LUT shading of gradient (gx, gy) to background (r, g, b).
 __device__ __forceinline__ void shade_one(const FrameParams& p, float gx, float gy, float& r,
                                           float& g, float& b) {

@@ -123,7 +123,16 @@ bool frame4_eligible(const FrameParams& p);
 cudaError_t launch_frame4(const FrameParams& p, cudaStream_t s);
 // band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
 bool frame5_eligible(const FrameParams& p);
-cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s);
+// Context-owned streams/events that pipeline chunk i's shading with chunk i+1's
+// blur (blurred scratch double-buffered).  null -> everything on the caller's stream.
+struct Overlap {
+  cudaStream_t blur, shade;
+  cudaEvent_t start, blur_done[2], shade_done[2], end;
+};
+// kt (nullable, diagnostics): accumulates the CUDA-event time of each kernel
+// kind [blur, shade, epilogue] in ms (synchronises the stream per launch).
+cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, const Overlap* ov, float* kt = nullptr);
+int frame5_launches(const FrameParams& p, long long n_env);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,
                                cudaStream_t s);
 cudaError_t launch_normals(const float* elev, float* normals, int H, int W, float inv_p,

@@ -162,5 +162,17 @@ class TactilePipeline:
         _lib.check(self.ctx.lib.tac_pipeline(self.ctx.handle, ctypes.byref(args), self.ctx.stream()),
                    "tac_pipeline")
 
+    def launches_per_call(self, n_env):
+        """Kernel launches one tac_pipeline call makes (diagnostics)."""
+        return int(self.ctx.lib.tac_pipeline_launches(self.ctx.handle, int(n_env)))
+
+    def profile(self, args, iters=10):
+        """Mean per-call CUDA-event milliseconds of each kernel kind
+        [blur (or the fused frame kernel), shade, per-env epilogue]."""
+        ms = (ctypes.c_float * 3)()
+        _lib.check(self.ctx.lib.tac_pipeline_profile(self.ctx.handle, ctypes.byref(args), self.ctx.stream(),
+                                                     int(iters), ms), "tac_pipeline_profile")
+        return [float(v) for v in ms]
+
 
 __all__ = ["TactilePipeline", "Observation", "SUMMARY_FIELDS", "_ptr"]
