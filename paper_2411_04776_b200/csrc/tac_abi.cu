@@ -19,6 +19,8 @@ struct tac_ctx {
   int device;
   float4* d_lut = nullptr;
   float* d_bg = nullptr;
+  float4* d_lut_planar = nullptr;  // [4][bins] float4: plane j = float4 j of every bin (v5 shading)
+  float* d_bg_planar = nullptr;    // [3][H*W]: R, G, B background planes (v5 shading)
   uint8_t* d_bg_u8 = nullptr;
   double* d_grid = nullptr;
   int2* d_shadow_off = nullptr;
@@ -162,6 +164,8 @@ int free_ctx(tac_ctx* c) {
     if (ev) cudaEventDestroy(ev);
   cudaFree(c->d_lut);
   cudaFree(c->d_bg);
+  cudaFree(c->d_lut_planar);
+  cudaFree(c->d_bg_planar);
   cudaFree(c->d_bg_u8);
   cudaFree(c->d_grid);
   cudaFree(c->d_shadow_off);
@@ -268,6 +272,15 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   for (size_t b = 0; b < nbins; ++b)
     for (int ch = 0; ch < 3; ++ch)
       for (int t = 1; t < 6; ++t) lut[b * 16 + ch * 5 + (t - 1)] = k.lut[(b * 3 + ch) * 6 + t];
+  // planar copies for the band shading kernel: a warp's gathers of float4 j of
+  // 32 nearby bins fall on 8-bin lines, and background loads are coalesced
+  std::vector<float> lutp(lut.size());
+  for (size_t b = 0; b < nbins; ++b)
+    for (int j = 0; j < 4; ++j)
+      for (int q = 0; q < 4; ++q) lutp[(j * nbins + b) * 4 + q] = lut[b * 16 + j * 4 + q];
+  std::vector<float> bgp(HW * 3);
+  for (size_t i = 0; i < HW; ++i)
+    for (int ch = 0; ch < 3; ++ch) bgp[ch * HW + i] = k.background[i * 3 + ch];
   std::vector<uint8_t> bgq(HW * 3);
   for (size_t i = 0; i < HW * 3; ++i) {
     long v = std::lrint((double)k.background[i]);  // half-to-even (default rounding mode)
@@ -294,6 +307,8 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
       {(void**)&c->d_lut, lut.data(), lut.size() * sizeof(float)},
       {(void**)&c->d_bg, k.background, HW * 3 * sizeof(float)},
       {(void**)&c->d_bg_u8, bgq.data(), bgq.size()},
+      {(void**)&c->d_lut_planar, lutp.data(), lutp.size() * sizeof(float)},
+      {(void**)&c->d_bg_planar, bgp.data(), bgp.size() * sizeof(float)},
       {(void**)&c->d_grid, grid.data(), grid.size() * sizeof(double)},
   };
   for (auto& u : ups) {
@@ -416,6 +431,9 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.dir_bins = k.dir_bins;
   b.lut = c->d_lut;
   b.bg = c->d_bg;
+  b.lut_planar = c->d_lut_planar;
+  b.bg_planar = c->d_bg_planar;
+  b.nbins = (int)nbins;
   b.bg_u8 = c->d_bg_u8;
   b.mg = mg;
 

@@ -377,11 +377,12 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
                     gys[0] == 0.f && gys[1] == 0.f && gys[2] == 0.f && gys[3] == 0.f;
   if (flat && p.shadow == nullptr) return false;
   const long long HW = (long long)H * W;
-  const float* bgp = p.bg + ((long long)y * W + xg) * 3;
-  const float4 b0 = __ldg(reinterpret_cast<const float4*>(bgp));
-  const float4 b1 = __ldg(reinterpret_cast<const float4*>(bgp) + 1);
-  const float4 b2 = __ldg(reinterpret_cast<const float4*>(bgp) + 2);
-  const float bgv[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+  // background planes: three coalesced 16-B loads per thread
+  const long long pix = (long long)y * W + xg;
+  const float4 br = __ldg(reinterpret_cast<const float4*>(p.bg_planar + pix));
+  const float4 bgr = __ldg(reinterpret_cast<const float4*>(p.bg_planar + HW + pix));
+  const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bg_planar + 2 * HW + pix));
+  const float bgv[12] = {br.x, bgr.x, bb.x, br.y, bgr.y, bb.y, br.z, bgr.z, bb.z, br.w, bgr.w, bb.w};
   float sf[4] = {1.f, 1.f, 1.f, 1.f};
   if (p.shadow) {
     const float4 f4 = __ldg(reinterpret_cast<const float4*>(p.shadow + env * HW + (long long)y * W + xg));
@@ -392,8 +393,14 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
   for (int h = 0; h < 2; ++h) {
     const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
     const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
-    const float4 a0 = __ldg(a0p.lut), c0 = __ldg(a0p.lut + 1), d0 = __ldg(a0p.lut + 2), e0 = __ldg(a0p.lut + 3);
-    const float4 a1 = __ldg(a1p.lut), c1 = __ldg(a1p.lut + 1), d1 = __ldg(a1p.lut + 2), e1 = __ldg(a1p.lut + 3);
+    // planar LUT: float4 j of bin b at lut_planar[j * nbins + b]
+    const int nb4 = p.nbins;
+    const long long i0 = (a0p.lut - p.lut) >> 2, i1 = (a1p.lut - p.lut) >> 2;  // bin indices
+    const float4* L = p.lut_planar;
+    const float4 a0 = __ldg(L + i0), c0 = __ldg(L + nb4 + i0), d0 = __ldg(L + 2 * nb4 + i0),
+                 e0 = __ldg(L + 3 * nb4 + i0);
+    const float4 a1 = __ldg(L + i1), c1 = __ldg(L + nb4 + i1), d1 = __ldg(L + 2 * nb4 + i1),
+                 e1 = __ldg(L + 3 * nb4 + i1);
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const Px& pp = s ? a1p : a0p;
@@ -444,6 +451,14 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   const int2 e1 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
   const int sa = min(e0.x, e1.x), sb = max(e0.y, e1.y);
   // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
+#ifdef TAC_K2_SPEC
+  // blurred rows loaded unconditionally, in parallel with the extent loads
+  // (the blurred scratch is written everywhere, zeros included)
+  float4 cc = *reinterpret_cast<const float4*>(rc);
+  float4 mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
+  float4 nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
+  const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
+#else
   const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
   float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
   if (any) {
@@ -451,6 +466,7 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
     mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
     nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
   }
+#endif
   float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
   float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
   bool done = false;

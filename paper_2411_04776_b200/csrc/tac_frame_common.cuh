@@ -181,6 +181,24 @@ __device__ __forceinline__ void add_lut(const float4 a, const float4 c, const fl
   b += d.z * nx + d.w * ny + e.x * nxx + e.y * nxy + e.z * nyy;
 }
 
+// Read-only 16-B loads with L1 allocation hints: LUT gathers are kept in L1
+// (evict_last), streamed operands (background, blurred rows) do not displace
+// them (no_allocate).
+__device__ __forceinline__ float4 ldg_keep(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+
 // Four quantised channel bytes -> one little-endian word (3 PRMT).
 __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x3340), __byte_perm(c, d, 0x3340), 0x5410);

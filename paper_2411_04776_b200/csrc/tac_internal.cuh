@@ -70,6 +70,9 @@ struct FrameParams {
   const float4* lut;     // [mag*dir][4] float4 = c1..c5 per channel (15 used)
   const float* bg;       // [H][W][3] 8-bit units
   const uint8_t* bg_u8;  // [H][W][3] = clamp(rint(bg))
+  const float4* lut_planar;  // [4][nbins]: plane j holds float4 j of every bin
+  const float* bg_planar;    // [3][H][W]
+  int nbins;
   // io
   const float* in;
   int input_depth;
