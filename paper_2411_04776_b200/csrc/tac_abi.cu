@@ -275,9 +275,21 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   // planar copies for the band shading kernel: a warp's gathers of float4 j of
   // 32 nearby bins fall on 8-bin lines, and background loads are coalesced
   std::vector<float> lutp(lut.size());
-  for (size_t b = 0; b < nbins; ++b)
+  // bin order of the planar LUT: 1 (default) = direction-major [dir][mag] (a
+  // 128-B line holds 8 magnitude bins of one direction: measured the most
+  // coherent for neighbouring pixels); 0 = [mag][dir]; 2 = 4 mag x 2 dir tiles
+  const int order = env_int("TAC_LUT_ORDER", 1);
+  const size_t mtiles = ((size_t)k.mag_bins + 3) / 4;
+  const size_t nbins_p = order == 2 ? mtiles * 4 * (((size_t)k.dir_bins + 1) / 2 * 2) : nbins;
+  lutp.assign(nbins_p * 16, 0.f);
+  for (size_t b = 0; b < nbins; ++b) {
+    const size_t mb = b / k.dir_bins, db = b % k.dir_bins;
+    size_t o = b;
+    if (order == 1) o = db * k.mag_bins + mb;
+    if (order == 2) o = ((db / 2) * mtiles + mb / 4) * 8 + (db % 2) * 4 + mb % 4;
     for (int j = 0; j < 4; ++j)
-      for (int q = 0; q < 4; ++q) lutp[(j * nbins + b) * 4 + q] = lut[b * 16 + j * 4 + q];
+      for (int q = 0; q < 4; ++q) lutp[(j * nbins_p + o) * 4 + q] = lut[b * 16 + j * 4 + q];
+  }
   std::vector<float> bgp(HW * 3);
   for (size_t i = 0; i < HW; ++i)
     for (int ch = 0; ch < 3; ++ch) bgp[ch * HW + i] = k.background[i * 3 + ch];
@@ -433,7 +445,8 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.bg = c->d_bg;
   b.lut_planar = c->d_lut_planar;
   b.bg_planar = c->d_bg_planar;
-  b.nbins = (int)nbins;
+  b.nbins = (int)nbins_p;
+  b.lut_order = order;
   b.bg_u8 = c->d_bg_u8;
   b.mg = mg;
 

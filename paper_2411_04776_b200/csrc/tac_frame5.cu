@@ -337,6 +337,12 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   for (int i = 0; i < 6; ++i) q[i] = t[i];
 }
 
+__device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) {
+  if (p.lut_order == 1) return db * p.mag_bins + mb;
+  if (p.lut_order == 2) return (((db >> 1) * ((p.mag_bins + 3) >> 2) + (mb >> 2)) << 3) + ((db & 1) << 2) + (mb & 3);
+  return mb * p.dir_bins + db;
+}
+
 // ---------------------------------------------------------------------------
 // kernel (b): shade one 4-pixel group of row y from its blurred rows (c = row
 // y with left/right neighbours, m = row y-1, n = row y+1; border rows/columns
@@ -395,7 +401,9 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
     const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
     // planar LUT: float4 j of bin b at lut_planar[j * nbins + b]
     const int nb4 = p.nbins;
-    const long long i0 = (a0p.lut - p.lut) >> 2, i1 = (a1p.lut - p.lut) >> 2;  // bin indices
+    // bin index in the planar order (see tac_abi.cu: lut_order)
+    const int i0 = planar_bin(p, a0p.mb, a0p.db);
+    const int i1 = planar_bin(p, a1p.mb, a1p.db);
     const float4* L = p.lut_planar;
     const float4 a0 = __ldg(L + i0), c0 = __ldg(L + nb4 + i0), d0 = __ldg(L + 2 * nb4 + i0),
                  e0 = __ldg(L + 3 * nb4 + i0);

@@ -154,6 +154,7 @@ __device__ __forceinline__ uint32_t u8sat(float v) {
 struct Px {
   const float4* lut;
   float nx, ny;
+  int mb, db;  // magnitude / direction bin
 };
 
 __device__ __forceinline__ Px bin_px(const FrameParams& p, float gx, float gy) {
@@ -167,7 +168,9 @@ __device__ __forceinline__ Px bin_px(const FrameParams& p, float gx, float gy) {
   int db = (int)((atan2_nz(gy, gx) + kPi) * p.dir_scale);  // NaN for (0,0) -> 0
   db = db >= p.dir_bins ? db - p.dir_bins : db;
   db = max(db, 0);
-  o.lut = p.lut + (max(mb, 0) * p.dir_bins + db) * 4;  // < 2^31 / 4 bins (host-checked)
+  o.mb = max(mb, 0);
+  o.db = db;
+  o.lut = p.lut + (o.mb * p.dir_bins + db) * 4;  // < 2^31 / 4 bins (host-checked)
   return o;
 }
 

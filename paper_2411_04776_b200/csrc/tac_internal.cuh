@@ -73,6 +73,7 @@ struct FrameParams {
   const float4* lut_planar;  // [4][nbins]: plane j holds float4 j of every bin
   const float* bg_planar;    // [3][H][W]
   int nbins;
+  int lut_order;             // lut_planar bin order: 0 = [mag][dir], 1 = [dir][mag], 2 = 4x2 tiles
   // io
   const float* in;
   int input_depth;
