@@ -97,16 +97,31 @@ __device__ __forceinline__ void h5fast(const float2* __restrict__ w, const float
   }
 }
 
-// Frame-border chunks: the window leaves the frame; column indices are
-// clamped (replicate border, scipy mode="nearest").  Same FFMA2 body.
-template <int RL>
-__device__ __forceinline__ void h5edge(const float2* __restrict__ w, const float* __restrict__ row0,
-                                       int c0, int W, float2 acc[8]) {
+// Frame-border chunks (the first and the last 16 columns; W % 16 == 0 and
+// RL4 <= 16 make these the only ones whose window leaves the frame): the
+// in-frame float4s are loaded as in h5fast and the out-of-frame columns take
+// the border value (replicate border, scipy mode="nearest").  `src` = vb row at
+// column c0 - RL4 (the out-of-frame part is never read).
+template <int RL, bool LEFT, bool RIGHT>
+__device__ __forceinline__ void h5edge(const float2* __restrict__ w, const float* __restrict__ src,
+                                       float2 acc[8]) {
   constexpr int RL4 = (RL + 3) & ~3;
   constexpr int NV = 16 + 2 * RL4;
   float v[NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = row0[min(max(c0 - RL4 + i, 0), W - 1)];
+  for (int q = 0; q < NV / 4; ++q) {
+    if ((LEFT && 4 * q < RL4) || (RIGHT && 4 * q >= 16 + RL4)) continue;
+    const float4 f = *reinterpret_cast<const float4*>(src + 4 * q);
+    v[4 * q] = f.x;
+    v[4 * q + 1] = f.y;
+    v[4 * q + 2] = f.z;
+    v[4 * q + 3] = f.w;
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (LEFT && i < RL4) v[i] = v[RL4];
+    if (RIGHT && i >= 16 + RL4) v[i] = v[15 + RL4];
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
 #pragma unroll
@@ -263,7 +278,7 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     const int c_lo = max(ha - R4, 0);
     const int c_hi = min(hb + R4, W - 1);
     const int np = (c_hi - c_lo) / 2 + 1;
-    const bool fast = c0 - R4 >= 0 && c0 + 15 + R4 <= W - 1;
+    const bool fast = c0 > 0 && c0 + 16 < W;  // interior chunk: window inside the frame (R4 <= 16)
     for (int l = 0; l < p.n_levels; ++l) {
       const int RL = p.radius[l];
       if (RL == 0) {  // identity level (k == 1): straight from the input
@@ -302,8 +317,12 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   case r:                                                                      \
     if (fast)                                                                  \
       h5fast<r>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc);         \
+    else if (c0 == 0 && c0 + 16 == W)                                          \
+      h5edge<r, true, true>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc); \
+    else if (c0 == 0)                                                          \
+      h5edge<r, true, false>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc); \
     else                                                                       \
-      h5edge<r>(p.wh2[l], vrow - vbase, c0, W, acc);                           \
+      h5edge<r, false, true>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc); \
     break;
           TAC5_RADIUS_CASES(X)
 #undef X
