@@ -175,9 +175,14 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   __syncthreads();
   if (tid == 0) {
     mbar_expect_tx(&s_bar, row_bytes * (unsigned)nrows);
-    for (int i = 0; i < nrows; ++i) {
-      const int cr = min(max(y0 - R + i, 0), H - 1);
-      bulk_g2s(inb + i * ip, src + (long long)cr * W, row_bytes, &s_bar);
+    if (y0 - R >= 0 && y0 + BH + R <= H && ip == W) {
+      // interior band: the 16 + 2R rows are one contiguous block
+      bulk_g2s(inb, src + (long long)(y0 - R) * W, row_bytes * (unsigned)nrows, &s_bar);
+    } else {
+      for (int i = 0; i < nrows; ++i) {
+        const int cr = min(max(y0 - R + i, 0), H - 1);
+        bulk_g2s(inb + i * ip, src + (long long)cr * W, row_bytes, &s_bar);
+      }
     }
   }
 
