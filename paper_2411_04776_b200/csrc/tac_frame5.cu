@@ -97,41 +97,6 @@ __device__ __forceinline__ void h5fast(const float2* __restrict__ w, const float
   }
 }
 
-// Frame-border chunks (the first and the last 16 columns; W % 16 == 0 and
-// RL4 <= 16 make these the only ones whose window leaves the frame): the
-// in-frame float4s are loaded as in h5fast and the out-of-frame columns take
-// the border value (replicate border, scipy mode="nearest").  `src` = vb row at
-// column c0 - RL4 (the out-of-frame part is never read).
-template <int RL, bool LEFT, bool RIGHT>
-__device__ __forceinline__ void h5edge(const float2* __restrict__ w, const float* __restrict__ src,
-                                       float2 acc[8]) {
-  constexpr int RL4 = (RL + 3) & ~3;
-  constexpr int NV = 16 + 2 * RL4;
-  float v[NV];
-#pragma unroll
-  for (int q = 0; q < NV / 4; ++q) {
-    if ((LEFT && 4 * q < RL4) || (RIGHT && 4 * q >= 16 + RL4)) continue;
-    const float4 f = *reinterpret_cast<const float4*>(src + 4 * q);
-    v[4 * q] = f.x;
-    v[4 * q + 1] = f.y;
-    v[4 * q + 2] = f.z;
-    v[4 * q + 3] = f.w;
-  }
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    if (LEFT && i < RL4) v[i] = v[RL4];
-    if (RIGHT && i >= 16 + RL4) v[i] = v[15 + RL4];
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-#pragma unroll
-    for (int t = -RL; t <= RL; ++t) {
-      const int a = RL4 + 2 * i + t;
-      acc[i] = ffma2(w[t < 0 ? -t : t], make_float2(v[a], v[a + 1]), acc[i]);
-    }
-  }
-}
-
 #define TAC5_RADIUS_CASES(X) \
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
@@ -283,7 +248,6 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     const int c_lo = max(ha - R4, 0);
     const int c_hi = min(hb + R4, W - 1);
     const int np = (c_hi - c_lo) / 2 + 1;
-    const bool fast = c0 > 0 && c0 + 16 < W;  // interior chunk: window inside the frame (R4 <= 16)
     for (int l = 0; l < p.n_levels; ++l) {
       const int RL = p.radius[l];
       if (RL == 0) {  // identity level (k == 1): straight from the input
@@ -316,18 +280,24 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
       }
       __syncthreads();
       if (has) {
-        const float* vrow = vb + row * vp;
+        float* vrow = vb + row * vp;
+        // frame-border chunks (the first / last 16 columns; W % 16 == 0 and
+        // R4 <= 16 make these the only windows that leave the frame): this
+        // thread writes its own row's replicate pads (scipy mode="nearest")
+        // and is the only reader of them
+        if (c0 == 0) {
+          const float e = vrow[-vbase];
+          for (int i = 0; i < R4; i += 4) *reinterpret_cast<float4*>(vrow + i) = make_float4(e, e, e, e);
+        }
+        if (c0 + 16 == W) {
+          const float e = vrow[W - 1 - vbase];
+          for (int i = 0; i < R4; i += 4)
+            *reinterpret_cast<float4*>(vrow + W - vbase + i) = make_float4(e, e, e, e);
+        }
         switch (RL) {
 #define X(r)                                                                   \
   case r:                                                                      \
-    if (fast)                                                                  \
-      h5fast<r>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc);         \
-    else if (c0 == 0 && c0 + 16 == W)                                          \
-      h5edge<r, true, true>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc); \
-    else if (c0 == 0)                                                          \
-      h5edge<r, true, false>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc); \
-    else                                                                       \
-      h5edge<r, false, true>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc); \
+    h5fast<r>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc);           \
     break;
           TAC5_RADIUS_CASES(X)
 #undef X
