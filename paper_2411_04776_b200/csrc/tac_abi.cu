@@ -119,9 +119,7 @@ void plan_v5(FrameParams& p) {
   p.bands = (p.H + 15) / 16;
   p.in_pitch = p.W;
   p.in_rows = 16 + 2 * p.R;
-  int vp = round_up(p.W + 2 * R4 + 4, 4);
-  if (((vp / 4) & 1) == 0) vp += 4;  // 4 x odd: LDS.128 over 8 rows is conflict-free
-  p.v_pitch = vp;
+  p.v_pitch = frame5_vpitch(p.W, R4);  // layout-dependent (tac_frame5.cu)
   p.b_pitch = 0;
   p.stage_bytes = 0;
 }

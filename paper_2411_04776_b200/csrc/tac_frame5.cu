@@ -13,23 +13,31 @@
 //     conversion pass clamps them (REF/tactile.py:193-197), folds the contact
 //     partials of REF/marker.py:109-121 (own rows only) and the band's
 //     non-zero column extent; then per level a vertical pass (column pair x 8
-//     rows per thread) and a horizontal pass (one row x 16 columns per thread,
-//     summed over levels in registers) write the blurred band to HBM/L2 with
-//     16-B stores.  Columns farther than R from any non-zero input are exactly
-//     0 and are not convolved (exact skip).
+//     rows per thread, writing a row-pair-interleaved intermediate) and a
+//     horizontal pass (row pair x 8 columns per thread: every FFMA2 operand is
+//     one aligned float2, summed over levels in registers) write the blurred
+//     band to HBM/L2 with 16-B stores.  Columns farther than R from any
+//     non-zero input are exactly 0 and are not convolved (exact skip).  The
+//     replicate pads of the first/last chunk are written by the thread that
+//     reads them.  Interior bands load their 16 + 2R rows with one bulk copy.
 //
-//  band_shade_kernel  kernel (b): 4 pixels per thread, ~40 warps per SM.  np.gradient differences (REF/optical.py:160), bins, binned-LUT
+//  band_shade_kernel  kernel (b): 4 pixels per thread, ~40 warps per SM.
+//     np.gradient differences (REF/optical.py:160), bins, binned-LUT
 //     shading (REF/optical.py:82-88, :244) + background, uint8 rule
 //     (REF/cli.py:134-139).  Pixels whose 3x3 blurred neighbourhood is zero
 //     (outside the band extents) are exactly rint(background) and copied.
+//     The LUT is read from a planar copy (float4 j of every bin in plane j,
+//     bins in direction-major order) and the background from R/G/B planes:
+//     the kernel is bound by L1 data-pipe wavefronts, and these layouts make a
+//     warp's 16-B gathers fall on far fewer 128-B lines.
 //
 //  env_epilogue_kernel  kernel (c): per env, reduces the band contact partials
 //     in a fixed order, finalises contact / summary / load
 //     (REF/marker.py:103-140), the marker displacements (REF/marker.py:143-165)
 //     and the dot splat (REF/marker.py:203-234).
 //
-// Envs run in chunks (TAC_CHUNK, default 256) so the blurred intermediate of a
-// chunk (256 x 307 KB = 79 MB at 240x320) stays resident in the 126 MB L2.
+// Envs run in chunks of TAC_CHUNK (default 4096): smaller chunks keep the
+// blurred intermediate in L2 but measured slower (launch tails dominate).
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -44,11 +52,13 @@ constexpr int BH = 16;    // band rows
 constexpr int K1T = 320;  // blur threads: 16 rows x 20 chunks of 16 columns
 constexpr int K2T = 320;  // shade threads
 
-// Vertical pass, one column pair x 8 output rows of one level.  `src` = input
-// row (first output row - RL), column c; every load feeds up to 8 FFMA2.
+// ---- row-pair interleaved intermediate ----------------------------------------
+// vb2[m][col] = (V[2m][col], V[2m+1][col]) as float2: the horizontal FFMA2
+// operand of output rows (2m, 2m+1) at column col + t is one aligned float2,
+// so no register re-pairing is needed.  Row-pair pitch (floats) = 4 x odd.
 template <int RL>
-__device__ __forceinline__ void v5item(const float2* __restrict__ w, const float* __restrict__ src,
-                                       int ip, float* __restrict__ dst, int vp, bool st_y) {
+__device__ __forceinline__ void v5item_rp(const float2* __restrict__ w, const float* __restrict__ src,
+                                          int ip, float* __restrict__ dst, int rpp) {
   float2 acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
@@ -61,39 +71,31 @@ __device__ __forceinline__ void v5item(const float2* __restrict__ w, const float
       if (t >= -RL && t <= RL) acc[k] = ffma2(w[t < 0 ? -t : t], v, acc[k]);
     }
   }
+  // rows (2m, 2m+1) of columns (c, c+1): one 16-B store per row pair
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    if (st_y)
-      *reinterpret_cast<float2*>(dst + k * vp) = acc[k];
-    else
-      dst[k * vp] = acc[k].x;
-  }
+  for (int m = 0; m < 4; ++m)
+    *reinterpret_cast<float4*>(dst + m * rpp) =
+        make_float4(acc[2 * m].x, acc[2 * m + 1].x, acc[2 * m].y, acc[2 * m + 1].y);
 }
 
-// Horizontal pass, one row x 16 columns (8 column pairs) of one level, fast
-// path: the window [c0 - RL4, c0 + 16 + RL4) lies inside the computed vb
-// columns; `src` = vb row at column c0 - RL4 (16-B aligned).
+// H for one row pair x 8 columns: acc[i] = (out[2m][c0+i], out[2m+1][c0+i]).
+// `src` = vb2 row pair at column c0 - RL4 (16-B aligned).
 template <int RL>
-__device__ __forceinline__ void h5fast(const float2* __restrict__ w, const float* __restrict__ src,
+__device__ __forceinline__ void h5pair(const float2* __restrict__ w, const float* __restrict__ src,
                                        float2 acc[8]) {
   constexpr int RL4 = (RL + 3) & ~3;
-  constexpr int NV = 16 + 2 * RL4;
-  float v[NV];
+  constexpr int NC = 8 + 2 * RL4;  // columns in the window
+  float2 v[NC];
 #pragma unroll
-  for (int q = 0; q < NV / 4; ++q) {
+  for (int q = 0; q < NC / 2; ++q) {
     const float4 f = *reinterpret_cast<const float4*>(src + 4 * q);
-    v[4 * q] = f.x;
-    v[4 * q + 1] = f.y;
-    v[4 * q + 2] = f.z;
-    v[4 * q + 3] = f.w;
+    v[2 * q] = make_float2(f.x, f.y);
+    v[2 * q + 1] = make_float2(f.z, f.w);
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
 #pragma unroll
-    for (int t = -RL; t <= RL; ++t) {
-      const int a = RL4 + 2 * i + t;
-      acc[i] = ffma2(w[t < 0 ? -t : t], make_float2(v[a], v[a + 1]), acc[i]);
-    }
+    for (int t = -RL; t <= RL; ++t) acc[i] = ffma2(w[t < 0 ? -t : t], v[RL4 + i + t], acc[i]);
   }
 }
 
@@ -235,16 +237,16 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     hb = 16 * k_hi + 15;
   }
   if (tid == 0) p.band_ext[env * nb + band] = make_int2(ha, hb);
-  const int row = tid & (BH - 1);
-  const int k = tid >> 4;
-  const int c0 = 16 * k;
-  const bool has = k >= k_lo && k <= k_hi;
+  // H items: row pair m x 8 columns; lanes 0..7 = row pairs of one chunk
+  const int m = tid & 7;
+  const int k8 = tid >> 3;
+  const int c0 = 8 * k8;
+  const bool has = k8 >= 2 * k_lo && k8 <= 2 * k_hi + 1 && c0 < W;
+  const int rpp = 2 * vp;  // floats per row pair (4 x odd)
   float2 acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
   if (ea <= eb) {
-    // V covers every in-frame column an H window of [ha, hb] reads (columns
-    // with no non-zero input within R come out as exact zeros)
     const int c_lo = max(ha - R4, 0);
     const int c_hi = min(hb + R4, W - 1);
     const int np = (c_hi - c_lo) / 2 + 1;
@@ -253,24 +255,22 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
       if (RL == 0) {  // identity level (k == 1): straight from the input
         if (has) {
           const float w = p.wh[l][0];
-          const float* in = inb + (row + R) * ip + c0;
+          const float* in0 = inb + (2 * m + R) * ip + c0;
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            acc[i] = ffma2(make_float2(w, w), make_float2(in[2 * i], in[2 * i + 1]), acc[i]);
+            acc[i] = ffma2(make_float2(w, w), make_float2(in0[i], in0[ip + i]), acc[i]);
         }
         continue;
       }
-      // V: one (column pair, 8-row half) item per thread
       if (tid < 2 * np) {
         const int hf = tid >= np ? 1 : 0;
         const int c = c_lo + 2 * (tid - hf * np);
-        const float* s = inb + (8 * hf + R - RL) * ip + c;
-        float* dst = vb + 8 * hf * vp + (c - vbase);
-        const bool st_y = c + 1 <= W - 1;
+        const float* sp = inb + (8 * hf + R - RL) * ip + c;
+        float* dst = vb + 4 * hf * rpp + 2 * (c - vbase);
         switch (RL) {
 #define X(r)                                            \
   case r:                                               \
-    v5item<r>(p.wv2[l], s, ip, dst, vp, st_y);          \
+    v5item_rp<r>(p.wv2[l], sp, ip, dst, rpp);           \
     break;
           TAC5_RADIUS_CASES(X)
 #undef X
@@ -280,24 +280,22 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
       }
       __syncthreads();
       if (has) {
-        float* vrow = vb + row * vp;
-        // frame-border chunks (the first / last 16 columns; W % 16 == 0 and
-        // R4 <= 16 make these the only windows that leave the frame): this
-        // thread writes its own row's replicate pads (scipy mode="nearest")
-        // and is the only reader of them
+        float* prow = vb + m * rpp;  // row pair m, column vbase
+        // frame-border chunks write their own row pair's replicate pads
         if (c0 == 0) {
-          const float e = vrow[-vbase];
-          for (int i = 0; i < R4; i += 4) *reinterpret_cast<float4*>(vrow + i) = make_float4(e, e, e, e);
+          const float2 e = *reinterpret_cast<const float2*>(prow - 2 * vbase);
+          for (int i = 0; i < R4; i += 2)
+            *reinterpret_cast<float4*>(prow + 2 * i) = make_float4(e.x, e.y, e.x, e.y);
         }
-        if (c0 + 16 == W) {
-          const float e = vrow[W - 1 - vbase];
-          for (int i = 0; i < R4; i += 4)
-            *reinterpret_cast<float4*>(vrow + W - vbase + i) = make_float4(e, e, e, e);
+        if (c0 + 8 == W) {
+          const float2 e = *reinterpret_cast<const float2*>(prow + 2 * (W - 1 - vbase));
+          for (int i = 0; i < R4; i += 2)
+            *reinterpret_cast<float4*>(prow + 2 * (W - vbase + i)) = make_float4(e.x, e.y, e.x, e.y);
         }
         switch (RL) {
 #define X(r)                                                                   \
   case r:                                                                      \
-    h5fast<r>(p.wh2[l], vrow + (c0 - ((r + 3) & ~3) - vbase), acc);           \
+    h5pair<r>(p.wh2[l], prow + 2 * (c0 - ((r + 3) & ~3) - vbase), acc);       \
     break;
           TAC5_RADIUS_CASES(X)
 #undef X
@@ -309,12 +307,19 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     }
   }
   // ---- blurred band out (exact zeros outside [ha, hb]) --------------------------
-  const int y = y0 + row;
-  if (k < nch && y < H) {
-    float4* d = reinterpret_cast<float4*>(p.scratch + env * HW + (long long)y * W + c0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      d[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x, acc[2 * i + 1].y);
+  {
+    const int y = y0 + 2 * m;
+    if (c0 < W) {
+      float* d = p.scratch + env * HW + (long long)y * W + c0;
+      if (y < H) {
+        reinterpret_cast<float4*>(d)[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+        reinterpret_cast<float4*>(d)[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);
+      }
+      if (y + 1 < H) {
+        reinterpret_cast<float4*>(d + W)[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+        reinterpret_cast<float4*>(d + W)[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
+      }
+    }
   }
 
   // ---- contact partials of the band (warp sums in s_red since the conversion;
@@ -517,6 +522,15 @@ __global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant
   const int nm = p.mg.rows * p.mg.cols;
   markers_block(p.mg, l, p.disp ? p.disp + env * (long long)nm * 2 : nullptr,
                 p.splat ? p.rgb + env * (long long)p.H * p.W * 3 : nullptr, nullptr, s_int, s_int + nm);
+}
+
+// vb pitch (floats per row): rows of W + 2 R4 columns; 2 x odd, so the
+// row-pair pitch (2 vp floats) is 4 x odd and LDS.128 over 8 row pairs is
+// conflict-free
+int frame5_vpitch(int W, int R4) {
+  int vp = ((W + 2 * R4 + 4 + 3) & ~3) + 2;  // 2 x odd -> row-pair pitch 4 x odd
+  if (((vp / 2) & 1) == 0) vp += 4;
+  return vp;
 }
 
 size_t band_blur_smem_bytes(const FrameParams& p) {

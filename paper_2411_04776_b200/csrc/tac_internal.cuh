@@ -137,6 +137,7 @@ struct Overlap {
 // kind [blur, shade, epilogue] in ms (synchronises the stream per launch).
 cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, const Overlap* ov, float* kt = nullptr);
 int frame5_launches(const FrameParams& p, long long n_env);
+int frame5_vpitch(int W, int R4);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,
                                cudaStream_t s);
 cudaError_t launch_normals(const float* elev, float* normals, int H, int W, float inv_p,
