@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
       v.w = clampf((p.rest - v.w) + p.rest_lo, 0.f, p.rest);
       *e = v;
     }
-    nz |= (v.x != 0.f) | (v.y != 0.f) | (v.z != 0.f) | (v.w != 0.f);
+    // any non-zero bit pattern (a -0 only widens the extent: still exact)
+    nz |= (__float_as_uint(v.x) | __float_as_uint(v.y) | __float_as_uint(v.z) | __float_as_uint(v.w)) != 0u;
     return v;
   };
   for (int i = ro; i < R; i += cstep) clamp4(reinterpret_cast<float4*>(inb + i * ip) + cg);
@@ -189,16 +190,16 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     }
     const float4 c4 = clamp4(e);
     const float v[4] = {c4.x, c4.y, c4.z, c4.w};
-    float rowsum = 0.f;
+    float w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       red.mx = fmaxf(red.mx, v[k]);
       const bool in = v[k] > p.threshold;
-      const float w = in ? v[k] : 0.f;
+      w[k] = in ? v[k] : 0.f;
       red.cnt += in ? 1.f : 0.f;
-      colsum[k] += w;
-      rowsum += w;
+      colsum[k] += w[k];
     }
+    const float rowsum = (w[0] + w[1]) + (w[2] + w[3]);
     red.sw += (double)rowsum;
     red.swy = fma((double)rowsum, (double)(y0 + i) + 0.5 - (double)p.half_h, red.swy);
   }
