@@ -124,6 +124,15 @@ int32_t tac_pipeline_launches(const tac_ctx* ctx, int64_t n_env);
 int tac_pipeline_profile(const tac_ctx* ctx, const struct tac_pipeline_args* args, void* stream,
                          int32_t iters, float* kernel_ms);
 
+/* render_heightmap (REF/tactile.py:129-190): orthographic z-buffer of
+ * camera-frame triangles.  verts: fp64 [N][n_verts][3] (camera frame, one
+ * vertex set per env), tris: int32 [n_tris][3] shared by every env (indices
+ * < n_verts, not checked on the device), depth out: fp32 [N][H][W] =
+ * fp32(reference float64 depth) -- rest where no triangle is hit. */
+int tac_render_heightmap(const tac_ctx* ctx, const double* verts, int64_t n_verts,
+                         const int32_t* tris, int64_t n_tris, float* depth,
+                         int64_t n_env, void* stream);
+
 /* indentation_from (REF/tactile.py:193-197): ind = clip(rest - depth, 0, rest).
  * depth, ind: [N,H,W]. */
 int tac_indentation(const tac_ctx* ctx, const float* depth, float* ind,

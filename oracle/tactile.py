@@ -113,3 +113,49 @@ def smooth_pyramid(ind, levels):
         else:
             acc += gaussian_blur(a, sigma, radius)
     return acc / len(levels)
+
+
+def render_heightmap(verts_cam, tris, h, w, pitch, rest):
+    """Orthographic z-buffer of camera-frame triangles (TEST INFRASTRUCTURE).
+
+    Restates tactile.py:129-150 and the per-triangle raster of
+    tactile.py:153-190 in float64: triangles whose nearest vertex is beyond
+    the rest surface or whose bounding box misses the sensing window are
+    culled; nearly edge-on triangles (|det| < 1e-18) are skipped; a pixel
+    centre ((j + 0.5 - w/2) p, (i + 0.5 - h/2) p) is covered when all three
+    barycentrics are >= -1e-12; covered hits with z <= rest lower the depth,
+    which starts at rest everywhere.  The arithmetic is written in the same
+    operation order as the reference so the result matches it bit for bit.
+    """
+    v = np.asarray(verts_cam, dtype=np.float64)
+    t = np.asarray(tris, dtype=np.int64)
+    depth = np.full((h, w), float(rest))
+    if t.size == 0:
+        return depth
+    c = v[t]  # (m, 3 corners, xyz)
+    hw, hh = 0.5 * w * pitch, 0.5 * h * pitch
+    x, y, z = c[..., 0], c[..., 1], c[..., 2]
+    live = ((z.min(1) <= rest) & (x.max(1) >= -hw) & (x.min(1) <= hw)
+            & (y.max(1) >= -hh) & (y.min(1) <= hh))
+    for k in np.flatnonzero(live):
+        (x0, y0, z0), (x1, y1, z1), (x2, y2, z2) = c[k]
+        det = (y1 - y2) * (x0 - x2) + (x2 - x1) * (y0 - y2)
+        if abs(det) < 1e-18:
+            continue
+        lo_j = max(0, int(np.ceil(min(x0, x1, x2) / pitch + 0.5 * w - 0.5)))
+        hi_j = min(w - 1, int(np.floor(max(x0, x1, x2) / pitch + 0.5 * w - 0.5)))
+        lo_i = max(0, int(np.ceil(min(y0, y1, y2) / pitch + 0.5 * h - 0.5)))
+        hi_i = min(h - 1, int(np.floor(max(y0, y1, y2) / pitch + 0.5 * h - 0.5)))
+        if hi_j < lo_j or hi_i < lo_i:
+            continue
+        cx = (np.arange(lo_j, hi_j + 1) + 0.5 - 0.5 * w) * pitch
+        cy = (np.arange(lo_i, hi_i + 1) + 0.5 - 0.5 * h) * pitch
+        px, py = cx[None, :], cy[:, None]
+        b0 = ((y1 - y2) * (px - x2) + (x2 - x1) * (py - y2)) / det
+        b1 = ((y2 - y0) * (px - x2) + (x0 - x2) * (py - y2)) / det
+        b2 = 1.0 - b0 - b1
+        zz = b0 * z0 + b1 * z1 + b2 * z2
+        ok = (b0 >= -1e-12) & (b1 >= -1e-12) & (b2 >= -1e-12) & (zz <= rest)
+        win = depth[lo_i:hi_i + 1, lo_j:hi_j + 1]
+        win[ok] = np.minimum(win[ok], zz[ok])
+    return depth

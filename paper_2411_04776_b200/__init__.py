@@ -3,7 +3,10 @@
 Batched, drop-in mirrors of the reference sensing API (REF/__init__.py:59-81)
 backed by hand-written sm_100a kernels in ``libtac_b200.so``:
 
-* ``TactilePipeline.simulate`` — the fused hot path (one launch per step).
+* ``TactilePipeline.simulate`` — the hot path: one ``tac_pipeline`` call per
+  step (band blur + shade kernels and a per-env epilogue).
+* ``render_heightmap`` / ``render_heightmaps`` — the mesh -> depth z-buffer
+  that feeds it (row f2).
 * ``indentation_from``, ``smooth_pyramid`` (tactile), ``normals_from``,
   ``shade`` (optical), ``contact_center``, ``track_load``,
   ``marker_displacements``, ``render_markers`` (marker) — the individual
@@ -38,6 +41,8 @@ _LAZY = {
     "indentation_from": ".tactile",
     "smooth_pyramid": ".tactile",
     "contact_blur": ".tactile",
+    "render_heightmap": ".tactile",
+    "render_heightmaps": ".tactile",
     "normals_from": ".optical",
     "shade": ".optical",
     "lut_from_polytable": ".optical",

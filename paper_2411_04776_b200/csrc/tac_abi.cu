@@ -510,6 +510,20 @@ int tac_set_profile_buffer(tac_ctx* c, int64_t* buf, int64_t n_env) {
   return TAC_OK;
 }
 
+int tac_render_heightmap(const tac_ctx* c, const double* verts, int64_t n_verts, const int32_t* tris,
+                         int64_t n_tris, float* depth, int64_t n_env, void* stream) {
+  int st = common_checks(c, n_env);
+  if (st) return st;
+  if (n_verts < 0 || n_tris < 0) return fail(TAC_ERR_INVALID, "n_verts and n_tris must be >= 0");
+  if (n_tris > 0x7fffffff / 3) return fail(TAC_ERR_UNSUPPORTED, "too many triangles");
+  if (n_env && !depth) return fail(TAC_ERR_INVALID, "null depth buffer");
+  if (n_env && n_tris && (!verts || !tris)) return fail(TAC_ERR_INVALID, "null vertex or triangle buffer");
+  if (n_tris && n_verts == 0) return fail(TAC_ERR_INVALID, "triangles need vertices");
+  cudaError_t e = launch_raster(verts, n_verts, tris, (int)n_tris, depth, c->cfg.height, c->cfg.width,
+                                c->cfg.pixel_pitch, c->cfg.gel_thickness, n_env, (cudaStream_t)stream);
+  return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_render_heightmap");
+}
+
 int tac_indentation(const tac_ctx* c, const float* depth, float* ind, int64_t n_env, void* stream) {
   int st = common_checks(c, n_env);
   if (st) return st;

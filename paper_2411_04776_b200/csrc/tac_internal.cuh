@@ -119,6 +119,10 @@ struct ShadowParams {
 cudaError_t launch_shadow(const ShadowParams& s, const float* in, int input_depth, float* factor,
                           float* rgb, long long n_env, cudaStream_t st);
 
+// Row f2: render_heightmap z-buffer (tac_raster.cu)
+cudaError_t launch_raster(const double* verts, long long n_verts, const int* tris, int n_tris, float* depth,
+                          int H, int W, double pitch, double rest, long long n_env, cudaStream_t s);
+
 size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 // slot-ring fused kernel (tac_frame4.cu): R <= RB, TMA-aligned input

@@ -117,3 +117,78 @@ def contact_blur(depth: torch.Tensor, cfg, *, input_kind="depth", summary=True):
         "tac_contact_blur",
     )
     return out, summ
+
+
+def _camera_frame(points, sensor_pose):
+    """World -> camera frame like the reference (REF/tactile.py:141-146): the
+    inverse sensor pose applied as p @ R^T + t in float64.  ``sensor_pose``:
+    None (identity), an object with ``inverse().apply`` (e.g. a tacsim Pose),
+    or a 4x4 camera-to-world matrix."""
+    import numpy as np
+
+    p = np.asarray(points, dtype=np.float64)
+    if sensor_pose is None:
+        return p
+    if hasattr(sensor_pose, "inverse"):
+        return np.asarray(sensor_pose.inverse().apply(p), dtype=np.float64)
+    m = np.asarray(sensor_pose, dtype=np.float64)
+    if m.shape != (4, 4):
+        raise InvalidArgumentError("sensor_pose must be None, a Pose, or a 4x4 matrix")
+    rinv = m[:3, :3].T
+    return p @ rinv.T + (-(rinv @ m[:3, 3]))
+
+
+def render_heightmap(surfaces, sensor_pose, cfg) -> HeightMap:
+    """Orthographic z-buffer render, REF/tactile.py:129-190, on the GPU.
+
+    Mirrors the reference call for one sensor: ``surfaces`` is a sequence of
+    (vertices [V,3] world frame, triangles [T,3]) pairs; ``sensor_pose`` as in
+    ``_camera_frame``; ``cfg`` a SensorConfig or PipelineConfig.  Returns a
+    HeightMap [H, W] (fp32 on the GPU) equal to fp32 of the reference's
+    float64 depth.  Batched use: ``render_heightmaps``.
+    """
+    import numpy as np
+
+    sensor = getattr(cfg, "sensor", cfg)
+    verts, tris, base = [], [], 0
+    for item in surfaces:
+        if not (isinstance(item, (tuple, list)) and len(item) == 2):
+            raise InvalidArgumentError("surface must be (vertices, triangles)")
+        v = np.asarray(item[0], dtype=np.float64)
+        t = np.asarray(item[1], dtype=np.int64)
+        if v.ndim != 2 or v.shape[1] != 3:
+            raise InvalidArgumentError("surface vertices must be (n, 3)")
+        if t.ndim != 2 or t.shape[1] != 3:
+            raise InvalidArgumentError("surface triangles must be (m, 3)")
+        verts.append(_camera_frame(v, sensor_pose))
+        tris.append(t + base)
+        base += len(v)
+    v = np.concatenate(verts) if verts else np.zeros((0, 3))
+    t = np.concatenate(tris) if tris else np.zeros((0, 3), np.int64)
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    out = render_heightmaps(torch.as_tensor(v, device=dev)[None], torch.as_tensor(t, device=dev), sensor)
+    return HeightMap(out[0], sensor.pixel_pitch, validate=False)
+
+
+def render_heightmaps(verts: torch.Tensor, tris: torch.Tensor, sensor, out: Optional[torch.Tensor] = None):
+    """Batched z-buffer (kernel ``raster_kernel``): ``verts`` fp64 [N, V, 3]
+    camera-frame vertices (one set per env, e.g. one mesh at N poses),
+    ``tris`` [T, 3] shared triangle indices.  Returns depth fp32 [N, H, W]."""
+    sensor = getattr(sensor, "sensor", sensor)
+    h, w = sensor.image_size
+    if verts.dim() != 3 or verts.shape[-1] != 3:
+        raise InvalidArgumentError("verts must be [N, V, 3]")
+    if tris.dim() != 2 or tris.shape[-1] != 3:
+        raise InvalidArgumentError("tris must be [T, 3]")
+    n, nv = verts.shape[0], verts.shape[1]
+    if tris.numel() and (int(tris.min()) < 0 or int(tris.max()) >= nv):
+        raise InvalidArgumentError("triangle index out of range")
+    v = verts.to(torch.float64).contiguous()
+    t = tris.to(device=v.device, dtype=torch.int32).contiguous()
+    ctx = context_for(blur_config(h, w, sensor.pixel_pitch, sensor.gelpad_thickness, ((0.0, 0),)), v.device)
+    if out is None:
+        out = torch.empty((n, h, w), dtype=torch.float32, device=v.device)
+    require(out, "out", torch.float32, (n, h, w), ctx.device)
+    _lib.check(ctx.lib.tac_render_heightmap(ctx.handle, v.data_ptr(), nv, t.data_ptr(), t.shape[0],
+                                            out.data_ptr(), n, ctx.stream()), "tac_render_heightmap")
+    return out

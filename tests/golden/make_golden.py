@@ -247,6 +247,32 @@ def render_cases():
     return out
 
 
+def raster_cases():
+    """render_heightmap (tactile.py:129-190) on meshes at several poses: the
+    camera-frame vertices the reference rasterises and its depth maps."""
+    out = {}
+    ident = geo.Pose()
+    cases = []
+    sph = geo.icosphere_surface(1.2e-3, 3)
+    cases.append((sph.vertices + np.array([0.0, 0.0, REST - 4e-4 + 1.2e-3]), sph.triangles, ident))
+    cases.append((sph.vertices + np.array([3.1e-4, -2.2e-4, REST - 7e-4 + 1.2e-3]), sph.triangles, ident))
+    world = geo.Pose.from_rotvec([0.03, -0.02, 0.05], [0.4, -0.3, 0.9])
+    cases.append((world.apply(sph.vertices + np.array([1e-4, 0.0, REST - 5e-4 + 1.2e-3])), sph.triangles, world))
+    plate_v = np.array([[-1.0, -1.0, REST - 2e-4], [1.0, -1.0, REST - 2e-4], [1.0, 1.0, REST - 1e-4],
+                        [-1.0, 1.0, REST - 1e-4]]) * np.array([1e-3, 1e-3, 1.0])
+    cases.append((plate_v, np.array([[0, 1, 2], [0, 2, 3]]), ident))
+    cases.append((plate_v + np.array([0.0, 0.0, 5e-4]), np.array([[0, 1, 2], [0, 2, 3]]), ident))  # beyond rest
+    small = geo.icosphere_surface(2e-4, 2)
+    cases.append((small.vertices + np.array([-7e-4, 5e-4, REST - 1e-4 + 2e-4]), small.triangles, ident))
+    for k, (vw, tri, pose) in enumerate(cases):
+        hm = tac.render_heightmap([(vw, tri)], pose, CFG)
+        out[f"verts_cam_{k}"] = pose.inverse().apply(vw)
+        out[f"tris_{k}"] = np.asarray(tri, dtype=np.int32)
+        out[f"depth_{k}"] = hm.values
+    out["n_cases"] = np.array(len(cases))
+    return out
+
+
 def main():
     tact = tactile_cases()
     opt = optical_cases(tact)
@@ -254,6 +280,7 @@ def main():
     shad = shadow_cases(tact, opt)
     np.savez_compressed(os.path.join(OUT, "shadows.npz"), **shad)
     np.savez_compressed(os.path.join(OUT, "render.npz"), **render_cases())
+    np.savez_compressed(os.path.join(OUT, "raster.npz"), **raster_cases())
     np.savez_compressed(os.path.join(OUT, "tactile.npz"), **tact)
     np.savez_compressed(os.path.join(OUT, "optical.npz"), **opt)
     np.savez_compressed(os.path.join(OUT, "marker.npz"), **mark)

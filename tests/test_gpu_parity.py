@@ -475,3 +475,61 @@ class TestKernelVariants:
         # and a few envs against the oracle
         for i in range(0, n, 16):
             check_env(cfg, depth[i].numpy(), obs4, i, shear[i], twist[i])
+
+
+class TestRenderHeightmap:
+    """Row f2: the GPU z-buffer against the reference depth maps
+    (tests/golden/raster.npz): fp32 of the reference float64 depth, exactly."""
+
+    def _sensor(self):
+        return SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3)
+
+    def test_golden_cases_exact(self, golden):
+        from paper_2411_04776_b200 import render_heightmaps
+
+        g = golden("raster")
+        for k in range(int(g["n_cases"])):
+            v = torch.as_tensor(g[f"verts_cam_{k}"], device=DEV)[None]
+            t = torch.as_tensor(g[f"tris_{k}"], device=DEV)
+            d = render_heightmaps(v, t, self._sensor()).cpu().numpy()[0]
+            assert np.array_equal(d, g[f"depth_{k}"].astype(np.float32)), k
+
+    def test_batched_envs_and_triangle_order(self, golden):
+        from paper_2411_04776_b200 import render_heightmaps
+
+        g = golden("raster")
+        # the three sphere cases share one triangle list: one batched launch
+        v = torch.as_tensor(np.stack([g[f"verts_cam_{k}"] for k in (0, 1, 2)]), device=DEV)
+        t = g["tris_0"]
+        perm = np.random.default_rng(9).permutation(len(t))
+        for tt in (t, t[perm]):
+            d = render_heightmaps(v, torch.as_tensor(tt, device=DEV), self._sensor()).cpu().numpy()
+            for i, k in enumerate((0, 1, 2)):
+                assert np.array_equal(d[i], g[f"depth_{k}"].astype(np.float32)), (i, k)
+
+    def test_mirror_signature_and_empty_scene(self, golden):
+        from paper_2411_04776_b200 import render_heightmap
+
+        g = golden("raster")
+        hm = render_heightmap([], None, self._sensor())
+        assert torch.equal(hm.values, torch.full((48, 64), np.float32(4e-3), device=hm.values.device))
+        hm = render_heightmap([(g["verts_cam_3"], g["tris_3"])], None, self._sensor())
+        assert np.array_equal(hm.values.cpu().numpy(), g["depth_3"].astype(np.float32))
+
+    def test_render_then_pipeline_matches_oracle_chain(self, golden):
+        """mesh -> depth (GPU) -> tactile image (GPU) equals the oracle chain.
+
+        Golden case 0 (a sphere centred exactly on the middle marker) is left
+        out: there the reference's normal displacement of that marker is 0/0
+        (REF/marker.py:155-160) and takes the direction of float64 rounding
+        noise in its centroid (~1e-20 m); this path's sums cancel exactly."""
+        from paper_2411_04776_b200 import render_heightmaps
+
+        g = golden("raster")
+        cfg = small_config(48, 64)
+        v = torch.as_tensor(np.stack([g[f"verts_cam_{k}"] for k in (1, 2)]), device=DEV)
+        depth = render_heightmaps(v, torch.as_tensor(g["tris_0"], device=DEV), cfg)
+        shear, twist = synthetic.loads(2, 77)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        for i, k in enumerate((1, 2)):
+            check_env(cfg, g[f"depth_{k}"].astype(np.float32), obs, i, shear[i], twist[i])

@@ -159,3 +159,38 @@ class TestShadowsGolden:
     def test_flat_map_identity(self, golden):
         g = golden("shadows")
         assert np.array_equal(g["default_2"], g["rgb"])
+
+
+class TestRasterGolden:
+    """Row f2: oracle render_heightmap vs the reference's own depth maps
+    (tests/golden/raster.npz, REF/tactile.py:129-190), bit for bit."""
+
+    def test_cases_bit_exact(self, golden):
+        g = golden("raster")
+        for k in range(int(g["n_cases"])):
+            d = tactile.render_heightmap(g[f"verts_cam_{k}"], g[f"tris_{k}"], 48, 64, 2.66e-5, 4e-3)
+            assert np.array_equal(d, g[f"depth_{k}"]), k
+
+    def test_empty_scene_is_rest(self):
+        d = tactile.render_heightmap(np.zeros((0, 3)), np.zeros((0, 3), np.int64), 8, 10, 1e-4, 4e-3)
+        assert np.array_equal(d, np.full((8, 10), 4e-3))
+
+    def test_triangle_order_invariance(self, golden):
+        g = golden("raster")
+        t = g["tris_0"]
+        perm = np.random.default_rng(3).permutation(len(t))
+        a = tactile.render_heightmap(g["verts_cam_0"], t, 48, 64, 2.66e-5, 4e-3)
+        b = tactile.render_heightmap(g["verts_cam_0"], t[perm], 48, 64, 2.66e-5, 4e-3)
+        assert np.array_equal(a, b)
+
+    def test_camera_frame_matrix_matches_pose_inverse(self):
+        from paper_2411_04776_b200.tactile import _camera_frame
+
+        rng = np.random.default_rng(5)
+        c, s = np.cos(0.3), np.sin(0.3)
+        m = np.eye(4)
+        m[:3, :3] = [[c, -s, 0], [s, c, 0], [0, 0, 1]]
+        m[:3, 3] = [0.1, -0.2, 0.3]
+        p = rng.normal(size=(20, 3))
+        back = _camera_frame(p @ m[:3, :3].T + m[:3, 3], m)
+        assert np.allclose(back, p, atol=1e-14)
