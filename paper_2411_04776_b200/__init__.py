@@ -7,6 +7,8 @@ backed by hand-written sm_100a kernels in ``libtac_b200.so``:
   step (band blur + shade kernels and a per-env epilogue).
 * ``render_heightmap`` / ``render_heightmaps`` — the mesh -> depth z-buffer
   that feeds it (row f2).
+* ``SensorObserver`` — N sensors stepped like ``Environment._observe``
+  (render -> pipeline with ``track_load`` on camera-pose deltas, row f3).
 * ``indentation_from``, ``smooth_pyramid`` (tactile), ``normals_from``,
   ``shade`` (optical), ``contact_center``, ``track_load``,
   ``marker_displacements``, ``render_markers`` (marker) — the individual
@@ -43,6 +45,8 @@ _LAZY = {
     "contact_blur": ".tactile",
     "render_heightmap": ".tactile",
     "render_heightmaps": ".tactile",
+    "SensorObserver": ".observer",
+    "pose_delta": ".observer",
     "normals_from": ".optical",
     "shade": ".optical",
     "lut_from_polytable": ".optical",

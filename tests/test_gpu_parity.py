@@ -533,3 +533,63 @@ class TestRenderHeightmap:
         obs = run_pipeline(cfg, depth, shear, twist)
         for i, k in enumerate((1, 2)):
             check_env(cfg, g[f"depth_{k}"].astype(np.float32), obs, i, shear[i], twist[i])
+
+
+class TestSensorObserver:
+    """Row f3: N sensors stepped like Environment._observe (REF/envs.py:1156-1209):
+    world meshes rendered from moving cameras, track_load on the camera-pose
+    deltas, against the oracle chain (render -> contact -> track_load ->
+    displacements) on the same poses."""
+
+    def test_moving_cameras_match_oracle(self, golden):
+        from scipy.spatial.transform import Rotation
+
+        from paper_2411_04776_b200 import SensorObserver
+
+        g = golden("raster")
+        cfg = small_config(48, 64)
+        n, steps = 3, 4
+        # (golden case 0, a press centred exactly on a marker, is singular: see
+        # TestRenderHeightmap.test_render_then_pipeline_matches_oracle_chain)
+        verts_cam0 = np.stack([g["verts_cam_1"], g["verts_cam_2"], g["verts_cam_1"] + [-1.7e-4, 0.9e-4, 1e-4]])
+        tris = g["tris_0"]
+        obsr = SensorObserver(cfg, n, DEV, keep_heightmap=True)
+        rng = np.random.default_rng(5)
+        mp = cfg.marker_params
+        params = (mp.k_n, mp.lambda_n, mp.lambda_s, mp.k_t, mp.lambda_t)
+        cams = [np.eye(4) for _ in range(n)]
+        ref_state = [dict(cx=0.0, cy=0.0, dmax=0.0, sx=0.0, sy=0.0, twist=0.0, in_contact=False)
+                     for _ in range(n)]
+        for t in range(steps):
+            if t:
+                for i in range(n):  # small in-plane camera motion + yaw
+                    step = np.eye(4)
+                    step[:3, :3] = Rotation.from_rotvec([0, 0, rng.uniform(-0.02, 0.02)]).as_matrix()
+                    step[:3, 3] = [rng.uniform(-3e-5, 3e-5), rng.uniform(-3e-5, 3e-5), 0.0]
+                    cams[i] = cams[i] @ step
+            cam = np.stack(cams)
+            # the world-frame scene is the step-0 camera-frame mesh
+            o = obsr.observe(torch.as_tensor(cam), verts_world=torch.as_tensor(verts_cam0),
+                             tris=torch.as_tensor(tris))
+            torch.cuda.synchronize()
+            for i in range(n):
+                vc = (verts_cam0[i] - cam[i, :3, 3]) @ cam[i, :3, :3]
+                d = otac.render_heightmap(vc, tris, 48, 64, cfg.pixel_pitch, synthetic.REST)
+                assert np.abs(o.heightmap[i].cpu().numpy() - d).max() <= 1e-9
+                ind = otac.indentation_from(o.heightmap[i].cpu().numpy().astype(np.float64), synthetic.REST)
+                c = omk.contact_center(ind, cfg.pixel_pitch)
+                if t:
+                    dlt = np.linalg.inv(prev[i]) @ cam[i]
+                    delta = (dlt[0, 3], dlt[1, 3], Rotation.from_matrix(dlt[:3, :3]).as_rotvec()[2])
+                else:
+                    delta = (0.0, 0.0, 0.0)
+                ref_state[i] = omk.track_load(ref_state[i], delta, c)
+                got = o.loads[i].cpu().numpy()
+                exp = [ref_state[i][k] for k in ("cx", "cy", "dmax", "sx", "sy", "twist")]
+                assert np.allclose(got[:6], exp, rtol=1e-5, atol=1e-9), (t, i, got, exp)
+                u = omk.marker_displacements(ref_state[i], cfg.rest_grid, params)
+                assert normwise(o.outputs.disp[i].cpu().numpy(), u) <= DISP_TOL
+            prev = cam.copy()
+        # masked reset zeroes one env's LoadState only
+        obsr.reset(torch.as_tensor(cam), mask=torch.tensor([True, False, False]))
+        assert not obsr.state[0].any() and obsr.state[1].any()
