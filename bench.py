@@ -336,7 +336,7 @@ def run_ours(a, rank, world, local_rank):
         shear_h = shear.cpu().pin_memory()
         twist_h = twist.cpu().pin_memory()
         out_h = host_observation(pipe, n_env)
-        streamer = HostStreamer(pipe, chunk=min(512, n_env))
+        streamer = HostStreamer(pipe, chunk=min(256, n_env))  # tools/e2e_sweep.py: best measured
         e_steps = max(3, min(20, a.steps // 10))
         for _ in range(2):
             streamer.run(depth_h, shear_h, twist_h, out_h)
@@ -362,6 +362,7 @@ def run_ours(a, rank, world, local_rank):
             "d2h_bytes_per_step": n_env * (3 * h * w + 8 * r * c + 32),
             "steps": e_steps,
             "path": "hostio.HostStreamer -> TactilePipeline.simulate (tac_pipeline C ABI), pinned host buffers",
+            "h2d_gbs": n_env * (4 * h * w + 16 + 8) * e_steps / (ems / 1e3) / 1e9,
         }
 
     if rank != 0:
