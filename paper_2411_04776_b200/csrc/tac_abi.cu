@@ -19,7 +19,7 @@ struct tac_ctx {
   int device;
   float4* d_lut = nullptr;
   float* d_bg = nullptr;
-  float4* d_lut_planar = nullptr;  // [4][bins] float4: plane j = float4 j of every bin (v5 shading)
+  float4* d_lut_half = nullptr;    // [2][bins][8] float: plane h = floats 8h..8h+7 of every bin (256-bit loads)
   float* d_bg_planar = nullptr;    // [3][H*W]: R, G, B background planes (v5 shading)
   uint8_t* d_bg_u8 = nullptr;
   double* d_grid = nullptr;
@@ -162,7 +162,7 @@ int free_ctx(tac_ctx* c) {
     if (ev) cudaEventDestroy(ev);
   cudaFree(c->d_lut);
   cudaFree(c->d_bg);
-  cudaFree(c->d_lut_planar);
+  cudaFree(c->d_lut_half);
   cudaFree(c->d_bg_planar);
   cudaFree(c->d_bg_u8);
   cudaFree(c->d_grid);
@@ -270,23 +270,22 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   for (size_t b = 0; b < nbins; ++b)
     for (int ch = 0; ch < 3; ++ch)
       for (int t = 1; t < 6; ++t) lut[b * 16 + ch * 5 + (t - 1)] = k.lut[(b * 3 + ch) * 6 + t];
-  // planar copies for the band shading kernel: a warp's gathers of float4 j of
-  // 32 nearby bins fall on 8-bin lines, and background loads are coalesced
-  std::vector<float> lutp(lut.size());
-  // bin order of the planar LUT: 1 (default) = direction-major [dir][mag] (a
-  // 128-B line holds 8 magnitude bins of one direction: measured the most
-  // coherent for neighbouring pixels); 0 = [mag][dir]; 2 = 4 mag x 2 dir tiles
+  // half-planar LUT for the band shading kernel (plane h = floats 8h..8h+7 of
+  // every bin, one 256-bit load each: a 128-B line holds 4 bins of a plane) and
+  // R/G/B background planes (coalesced loads).  Bin order: 1 (default) =
+  // direction-major [dir][mag] (neighbouring pixels' bins share lines most
+  // often: measured best); 0 = [mag][dir]; 2 = 4 mag x 2 dir tiles
   const int order = env_int("TAC_LUT_ORDER", 1);
   const size_t mtiles = ((size_t)k.mag_bins + 3) / 4;
   const size_t nbins_p = order == 2 ? mtiles * 4 * (((size_t)k.dir_bins + 1) / 2 * 2) : nbins;
-  lutp.assign(nbins_p * 16, 0.f);
+  std::vector<float> luth(nbins_p * 16, 0.f);
   for (size_t b = 0; b < nbins; ++b) {
     const size_t mb = b / k.dir_bins, db = b % k.dir_bins;
     size_t o = b;
     if (order == 1) o = db * k.mag_bins + mb;
     if (order == 2) o = ((db / 2) * mtiles + mb / 4) * 8 + (db % 2) * 4 + mb % 4;
-    for (int j = 0; j < 4; ++j)
-      for (int q = 0; q < 4; ++q) lutp[(j * nbins_p + o) * 4 + q] = lut[b * 16 + j * 4 + q];
+    for (int hh = 0; hh < 2; ++hh)
+      for (int q = 0; q < 8; ++q) luth[(hh * nbins_p + o) * 8 + q] = lut[b * 16 + hh * 8 + q];
   }
   std::vector<float> bgp(HW * 3);
   for (size_t i = 0; i < HW; ++i)
@@ -317,7 +316,7 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
       {(void**)&c->d_lut, lut.data(), lut.size() * sizeof(float)},
       {(void**)&c->d_bg, k.background, HW * 3 * sizeof(float)},
       {(void**)&c->d_bg_u8, bgq.data(), bgq.size()},
-      {(void**)&c->d_lut_planar, lutp.data(), lutp.size() * sizeof(float)},
+      {(void**)&c->d_lut_half, luth.data(), luth.size() * sizeof(float)},
       {(void**)&c->d_bg_planar, bgp.data(), bgp.size() * sizeof(float)},
       {(void**)&c->d_grid, grid.data(), grid.size() * sizeof(double)},
   };
@@ -441,7 +440,7 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.dir_bins = k.dir_bins;
   b.lut = c->d_lut;
   b.bg = c->d_bg;
-  b.lut_planar = c->d_lut_planar;
+  b.lut_half = reinterpret_cast<const float*>(c->d_lut_half);
   b.bg_planar = c->d_bg_planar;
   b.nbins = (int)nbins_p;
   b.lut_order = order;

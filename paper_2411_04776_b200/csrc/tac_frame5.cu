@@ -26,10 +26,11 @@
 //     shading (REF/optical.py:82-88, :244) + background, uint8 rule
 //     (REF/cli.py:134-139).  Pixels whose 3x3 blurred neighbourhood is zero
 //     (outside the band extents) are exactly rint(background) and copied.
-//     The LUT is read from a planar copy (float4 j of every bin in plane j,
-//     bins in direction-major order) and the background from R/G/B planes:
-//     the kernel is bound by L1 data-pipe wavefronts, and these layouts make a
-//     warp's 16-B gathers fall on far fewer 128-B lines.
+//     The LUT is read from a half-planar copy (plane h = floats 8h..8h+7 of
+//     every bin, bins in direction-major order) with two 256-bit loads per
+//     pixel, and the background from R/G/B planes: the kernel is bound by L1
+//     data-pipe wavefronts, and these layouts make a warp's gathers fall on
+//     far fewer 128-B lines.
 //
 //  env_epilogue_kernel  kernel (c): per env, reduces the band contact partials
 //     in a fixed order, finalises contact / summary / load
@@ -229,7 +230,6 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   const int ea = s_lo, eb = s_hi;
 
   // ---- blur: output range [ha, hb] in whole 16-column chunks ------------------
-  const int nch = W >> 4;
   int k_lo = 0, k_hi = -1, ha = INT_MAX, hb = INT_MIN;
   if (ea <= eb) {
     k_lo = max(ea - R, 0) >> 4;
@@ -337,6 +337,13 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   for (int i = 0; i < 6; ++i) q[i] = t[i];
 }
 
+// one 256-bit read-only load (LDG.E.ENL2.256 on sm_100a)
+__device__ __forceinline__ void ld256(const float* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+
 __device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) {
   if (p.lut_order == 1) return db * p.mag_bins + mb;
   if (p.lut_order == 2) return (((db >> 1) * ((p.mag_bins + 3) >> 2) + (mb >> 2)) << 3) + ((db & 1) << 2) + (mb & 3);
@@ -399,16 +406,14 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
   for (int h = 0; h < 2; ++h) {
     const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
     const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
-    // planar LUT: float4 j of bin b at lut_planar[j * nbins + b]
-    const int nb4 = p.nbins;
-    // bin index in the planar order (see tac_abi.cu: lut_order)
+    // two 256-bit loads per pixel: floats 0..7 and 8..15 of the bin
     const int i0 = planar_bin(p, a0p.mb, a0p.db);
     const int i1 = planar_bin(p, a1p.mb, a1p.db);
-    const float4* L = p.lut_planar;
-    const float4 a0 = __ldg(L + i0), c0 = __ldg(L + nb4 + i0), d0 = __ldg(L + 2 * nb4 + i0),
-                 e0 = __ldg(L + 3 * nb4 + i0);
-    const float4 a1 = __ldg(L + i1), c1 = __ldg(L + nb4 + i1), d1 = __ldg(L + 2 * nb4 + i1),
-                 e1 = __ldg(L + 3 * nb4 + i1);
+    float4 a0, c0, d0, e0, a1, c1, d1, e1;
+    ld256(p.lut_half + 8 * i0, a0, c0);
+    ld256(p.lut_half + 8 * (p.nbins + i0), d0, e0);
+    ld256(p.lut_half + 8 * i1, a1, c1);
+    ld256(p.lut_half + 8 * (p.nbins + i1), d1, e1);
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const Px& pp = s ? a1p : a0p;

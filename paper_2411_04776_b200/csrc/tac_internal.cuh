@@ -70,10 +70,10 @@ struct FrameParams {
   const float4* lut;     // [mag*dir][4] float4 = c1..c5 per channel (15 used)
   const float* bg;       // [H][W][3] 8-bit units
   const uint8_t* bg_u8;  // [H][W][3] = clamp(rint(bg))
-  const float4* lut_planar;  // [4][nbins]: plane j holds float4 j of every bin
+  const float* lut_half;     // [2][nbins][8]: plane h holds floats 8h..8h+7 of every bin
   const float* bg_planar;    // [3][H][W]
   int nbins;
-  int lut_order;             // lut_planar bin order: 0 = [mag][dir], 1 = [dir][mag], 2 = 4x2 tiles
+  int lut_order;             // lut_half bin order: 0 = [mag][dir], 1 = [dir][mag], 2 = 4x2 tiles
   // io
   const float* in;
   int input_depth;

@@ -7,7 +7,7 @@ make -s -j8 >/dev/null
 out=/tmp/ab_$1; mkdir -p $out
 NV="nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -ftz=true -Xcompiler -fPIC --expt-relaxed-constexpr"
 objs=""
-for f in tac_frame tac_frame4 tac_frame5 tac_small tac_shadow tac_abi; do
+for f in $(sed -n 's/^SRCS := //p' Makefile | sed 's/\.cu//g'); do
   if [ "$f" = "tac_frame5" ]; then $NV $2 -c $f.cu -o $out/$f.o; objs="$objs $out/$f.o"; else objs="$objs build/$f.o"; fi
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libtac_b200_$1.so $objs
