@@ -110,11 +110,6 @@ const char* tac_last_error(void);
 size_t tac_workspace_bytes(const tac_ctx* ctx, int64_t n_env);
 /* Tiles per frame used by the frame kernels (for diagnostics). */
 int32_t tac_tiles_per_frame(const tac_ctx* ctx);
-/* Diagnostics: device buffer of n_env * ceil(H/16) * 8 int64 that the fused
- * slot-ring kernel fills with per-row-block SM clock stamps of its blur and
- * shade groups for the first n_env envs of each tac_pipeline call (NULL = off).
- * Not thread-safe with concurrent tac_pipeline calls on the same context. */
-int tac_set_profile_buffer(tac_ctx* ctx, int64_t* buf, int64_t n_env);
 /* Diagnostics: number of kernel launches one tac_pipeline call makes for n_env. */
 int32_t tac_pipeline_launches(const tac_ctx* ctx, int64_t n_env);
 /* Diagnostics: runs tac_pipeline `iters` times with a CUDA event pair around

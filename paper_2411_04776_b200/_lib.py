@@ -93,7 +93,6 @@ SIGNATURES = {
     "tac_last_error": (ctypes.c_char_p, []),
     "tac_workspace_bytes": (ctypes.c_size_t, [_p, _i64]),
     "tac_tiles_per_frame": (_i32, [_p]),
-    "tac_set_profile_buffer": (ctypes.c_int, [_p, _p, _i64]),
     "tac_pipeline_launches": (_i32, [_p, _i64]),
     "tac_pipeline_profile": (ctypes.c_int, [_p, ctypes.POINTER(TacPipelineArgs), _p, _i32, _p]),
     "tac_render_heightmap": (ctypes.c_int, [_p, _p, _i64, _p, _i64, _p, _i64, _p]),

@@ -27,15 +27,11 @@ struct tac_ctx {
   float* d_shadow_cost = nullptr;
   ShadowParams shadow;
   FrameParams fused, blur, contact;  // per-mode launch templates
-  FrameParams fused4;                // slot-ring fused kernel geometry
-  bool use4;                         // fused4 is eligible (TAC_FRAME=4 selects it)
   FrameParams fused5;                // band-tiled two-kernel geometry (default)
   bool use5;
   long long chunk5;                  // envs per v5 launch pair
   bool overlap5;                     // pipeline chunks over two context streams
   Overlap ov{};                      // created with the context (overlap5)
-  long long* prof = nullptr;         // diagnostics buffer (tac_set_profile_buffer)
-  long long prof_envs = 0;
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
 };
@@ -93,23 +89,6 @@ void plan_strips(FrameParams& p, int mode, int max_strip) {
   p.b_pitch = bp;
   (void)0;
   p.stage_bytes = (RB + 1) * p.strip_w * 3;
-}
-
-// Geometry of the slot-ring fused kernel (see tac_frame4.cu): vb rows start at
-// column bx0 - round_up(R, 4) and are read as 16-column chunks (+/- RL4).
-void plan_v4(FrameParams& p) {
-  const int R4 = round_up(p.R, 4);
-  const int ring = p.strips > 1 ? 1 : 0;
-  const int ew = p.strip_w + 2 * ring + 3;
-  const int nch = (ew + 15) / 16;
-  int vp = round_up(16 * nch + 2 * R4 + 4, 4);
-  if (((vp / 4) & 1) == 0) vp += 4;  // 4 x odd: LDS.128 over 8 rows is conflict-free
-  p.v_pitch = vp;
-  int bp = round_up(ew + 16 + 4, 4);
-  if (((bp / 4) & 1) == 0) bp += 4;
-  p.b_pitch = bp;
-  p.in_rows = 3 * RB;  // input slot ring of blocks b-1..b+1
-  p.stage_bytes = 0;
 }
 
 // Geometry of the band-tiled path (see tac_frame5.cu): input rows of W floats,
@@ -455,10 +434,7 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   c->contact = b;
   plan_strips(c->contact, kModeContact, max_strip);
   c->max_tiles = std::max({c->fused.strips, c->blur.strips, c->contact.strips});
-  c->fused4 = c->fused;
-  plan_v4(c->fused4);
   const int kind = env_int("TAC_FRAME", 5);
-  c->use4 = kind == 4 && frame4_eligible(c->fused4);
   c->fused5 = c->fused;
   plan_v5(c->fused5);
   c->use5 = kind == 5 && frame5_eligible(c->fused5);
@@ -501,13 +477,6 @@ size_t tac_workspace_bytes(const tac_ctx* c, int64_t n_env) {
 
 int32_t tac_tiles_per_frame(const tac_ctx* c) { return c ? c->fused.strips : 0; }
 
-int tac_set_profile_buffer(tac_ctx* c, int64_t* buf, int64_t n_env) {
-  if (!c) return fail(TAC_ERR_INVALID, "null context");
-  if (n_env < 0 || (n_env > 0 && !buf)) return fail(TAC_ERR_INVALID, "bad profile buffer");
-  c->prof = n_env > 0 ? reinterpret_cast<long long*>(buf) : nullptr;
-  c->prof_envs = n_env;
-  return TAC_OK;
-}
 
 int tac_render_heightmap(const tac_ctx* c, const double* verts, int64_t n_verts, const int32_t* tris,
                          int64_t n_tris, float* depth, int64_t n_env, void* stream) {
@@ -651,9 +620,7 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
   }
   FrameParams p = c->fused;
   const bool tma = tma_ok(p, a->in);
-  const bool v4 = c->use4 && tma;
   const bool v5 = c->use5 && tma;
-  if (v4) p = c->fused4;
   if (v5) p = c->fused5;
   p.in = a->in;
   p.use_tma = tma;
@@ -672,8 +639,6 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
   p.disp = a->disp;
   p.splat = a->splat;
   p.shadow = a->shadow;
-  p.prof = c->prof;
-  p.prof_envs = c->prof_envs;
   cudaError_t e;
   if (v5) {
     bind_workspace5(c, p, a->workspace, a->n_env);
@@ -686,7 +651,7 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
       cudaEventCreate(&t1);
       cudaEventRecord(t0, (cudaStream_t)stream);
     }
-    e = v4 ? launch_frame4(p, (cudaStream_t)stream) : launch_frame(p, kModeFused, (cudaStream_t)stream);
+    e = launch_frame(p, kModeFused, (cudaStream_t)stream);
     if (kt) {
       cudaEventRecord(t1, (cudaStream_t)stream);
       cudaEventSynchronize(t1);

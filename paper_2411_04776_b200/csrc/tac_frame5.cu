@@ -1,10 +1,10 @@
 // Band-tiled two-kernel path (v5), the default tac_pipeline path for frames of
 // one strip (W <= 320, W % 16 == 0) with pyramid radii <= 16.
 //
-// Why two kernels: in the fused warp-specialised kernels (tac_frame.cu,
-// tac_frame4.cu) both the blur and the shade group run ~2.5 warps per SMSP
-// and every row block waits on the slower group; per-block clock stamps
-// (tools/phase_clock.py) showed both groups latency-bound at ~0.3 IPC.  Here
+// Why two kernels: in the fused warp-specialised kernel (tac_frame.cu, and a
+// slot-ring variant tried in round 1) both the blur and the shade group run
+// ~2.5 warps per SMSP and every row block waits on the slower group;
+// per-block clock64 stamps showed both groups latency-bound at ~0.3 IPC.  Here
 // each stage gets the occupancy it needs:
 //
 //  band_blur_kernel   kernel (a): one CTA per (env, 16-row band), 3 CTAs/SM.

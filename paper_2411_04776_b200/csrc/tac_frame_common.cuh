@@ -1,5 +1,5 @@
 // Device helpers shared by the frame kernels (tac_frame.cu: strip-streaming v3,
-// tac_frame4.cu: slot-ring v4): TMA/mbarrier and named-barrier wrappers, strip
+// tac_frame5.cu: band-tiled two-kernel path): TMA/mbarrier and named-barrier wrappers, strip
 // geometry, paired FMA, the shading arithmetic (bins, LUT basis, uint8 rule),
 // and the deterministic contact reductions + per-env finalisation.
 #pragma once

@@ -96,8 +96,6 @@ struct FrameParams {
   float* disp;           // nullable
   int splat;
   const float* shadow;   // nullable [N][H][W] multiplicative shadow factor
-  long long* prof;       // nullable diagnostics: [prof_envs][nblocks][8] clock64 stamps
-  long long prof_envs;
   // band-tiled two-kernel path (tac_frame5.cu)
   int bands;             // ceil(H / 16)
   long long chunk;       // envs per (blur, shade) launch pair
@@ -125,10 +123,6 @@ cudaError_t launch_raster(const double* verts, long long n_verts, const int* tri
 
 size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
-// slot-ring fused kernel (tac_frame4.cu): R <= RB, TMA-aligned input
-size_t frame4_smem_bytes(const FrameParams& p);
-bool frame4_eligible(const FrameParams& p);
-cudaError_t launch_frame4(const FrameParams& p, cudaStream_t s);
 // band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
 bool frame5_eligible(const FrameParams& p);
 // Context-owned streams/events that pipeline chunk i's shading with chunk i+1's
