@@ -30,8 +30,6 @@ struct tac_ctx {
   FrameParams fused5;                // band-tiled two-kernel geometry (default)
   bool use5;
   long long chunk5;                  // envs per v5 launch pair
-  bool overlap5;                     // pipeline chunks over two context streams
-  Overlap ov{};                      // created with the context (overlap5)
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
 };
@@ -111,9 +109,8 @@ size_t v5_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   if (!c->use5) return 0;
   const long long C = std::min<long long>(n_env, c->chunk5);
   const FrameParams& p = c->fused5;
-  const size_t halves = c->overlap5 ? 2 : 1;  // double-buffered scratch when chunks overlap
   return align256((size_t)n_env * p.bands * kSumFields * sizeof(double)) +
-         align256(halves * C * p.bands * sizeof(int2)) + align256(halves * C * p.H * p.W * sizeof(float));
+         align256((size_t)C * p.bands * sizeof(int2)) + align256((size_t)C * p.H * p.W * sizeof(float));
 }
 
 size_t v3_workspace_bytes(const tac_ctx* c, int64_t n_env) {
@@ -127,18 +124,13 @@ void bind_workspace5(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) 
   p.partials = reinterpret_cast<double*>(b);
   b += align256((size_t)n_env * p.bands * kSumFields * sizeof(double));
   p.band_ext = reinterpret_cast<int2*>(b);
-  b += align256((c->overlap5 ? 2 : 1) * (size_t)C * p.bands * sizeof(int2));
+  b += align256((size_t)C * p.bands * sizeof(int2));
   p.scratch = reinterpret_cast<float*>(b);
   p.chunk = C;
 }
 
 int free_ctx(tac_ctx* c) {
   if (!c) return TAC_OK;
-  if (c->ov.blur) cudaStreamDestroy(c->ov.blur);
-  if (c->ov.shade) cudaStreamDestroy(c->ov.shade);
-  for (cudaEvent_t ev : {c->ov.start, c->ov.blur_done[0], c->ov.blur_done[1], c->ov.shade_done[0],
-                         c->ov.shade_done[1], c->ov.end})
-    if (ev) cudaEventDestroy(ev);
   cudaFree(c->d_lut);
   cudaFree(c->d_bg);
   cudaFree(c->d_lut_half);
@@ -439,18 +431,6 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   plan_v5(c->fused5);
   c->use5 = kind == 5 && frame5_eligible(c->fused5);
   c->chunk5 = std::max(1, env_int("TAC_CHUNK", 4096));
-  c->overlap5 = c->use5 && env_int("TAC_OVERLAP", 0) != 0;  // measured slower: off by default
-  if (c->overlap5) {
-    cudaError_t e = cudaStreamCreateWithFlags(&c->ov.blur, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->ov.shade, cudaStreamNonBlocking);
-    for (cudaEvent_t* ev : {&c->ov.start, &c->ov.blur_done[0], &c->ov.blur_done[1], &c->ov.shade_done[0],
-                            &c->ov.shade_done[1], &c->ov.end})
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
-    if (e != cudaSuccess) {
-      free_ctx(c);
-      return cuda_fail(e, "overlap streams");
-    }
-  }
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
     if (p.stage_bytes > (int)(RB * p.v_pitch * sizeof(float))) {
@@ -642,7 +622,7 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
   cudaError_t e;
   if (v5) {
     bind_workspace5(c, p, a->workspace, a->n_env);
-    e = launch_frame5(p, (cudaStream_t)stream, c->overlap5 ? &c->ov : nullptr, kt);
+    e = launch_frame5(p, (cudaStream_t)stream, kt);
   } else {
     bind_workspace(c, p, a->workspace, a->n_env);
     cudaEvent_t t0 = nullptr, t1 = nullptr;

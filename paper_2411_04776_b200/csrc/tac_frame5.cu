@@ -586,7 +586,7 @@ struct KTimer {
   }
 };
 
-cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, const Overlap* ov, float* kt) {
+cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt) {
   const size_t smem = band_blur_smem_bytes(p0);
   cudaError_t e = cudaFuncSetAttribute(band_blur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -599,53 +599,31 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, const Overlap* 
   const unsigned nq = (unsigned)((p0.H + rpc - 1) / rpc);
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
   const long long nchunks = (p0.n_env + chunk - 1) / chunk;
-  // with overlap: blur on ov->blur, shading on ov->shade, scratch halves alternate
-  const bool two = ov != nullptr && nchunks > 1 && p0.blurred == nullptr && kt == nullptr;
   KTimer tm(kt, s);
-  cudaStream_t sb = two ? ov->blur : s, ss = two ? ov->shade : s;
 #define CK(x)                          \
   do {                                 \
     e = (x);                           \
     if (e != cudaSuccess) return e;    \
   } while (0)
-  if (two) {
-    CK(cudaEventRecord(ov->start, s));
-    CK(cudaStreamWaitEvent(sb, ov->start, 0));
-    CK(cudaStreamWaitEvent(ss, ov->start, 0));
-  }
   for (long long i = 0; i < nchunks; ++i) {
     const long long e0 = i * chunk;
     const long long n = std::min(chunk, p0.n_env - e0);
-    const int half = (int)(i & 1);
     FrameParams p = p0;
     // per-chunk views (every per-env pointer advanced by e0 envs)
     p.in = p0.in + e0 * HW;
     p.rgb = p0.rgb + e0 * HW * 3;
-    p.scratch = p0.blurred ? p0.blurred + e0 * HW : p0.scratch + (two ? half * chunk * HW : 0);
-    p.band_ext = p0.band_ext + (two ? half * chunk * p0.bands : 0);
+    p.scratch = p0.blurred ? p0.blurred + e0 * HW : p0.scratch;
     p.partials = p0.partials + e0 * p0.bands * kSumFields;
     if (p0.shadow) p.shadow = p0.shadow + e0 * HW;
     p.n_env = n;
-    if (two && i >= 2) CK(cudaStreamWaitEvent(sb, ov->shade_done[half], 0));  // scratch half is free
     tm.start();
-    band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, sb>>>(p);
+    band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
     CK(cudaGetLastError());
     tm.stop(0);
-    if (two) {
-      CK(cudaEventRecord(ov->blur_done[half], sb));
-      CK(cudaStreamWaitEvent(ss, ov->blur_done[half], 0));
-    }
     tm.start();
-    band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, ss>>>(p);
+    band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
     CK(cudaGetLastError());
     tm.stop(1);
-    if (two) CK(cudaEventRecord(ov->shade_done[half], ss));
-  }
-  if (two) {  // join: the epilogue needs every blur (partials) and every shade (RGB)
-    CK(cudaEventRecord(ov->end, sb));
-    CK(cudaStreamWaitEvent(s, ov->end, 0));
-    CK(cudaEventRecord(ov->end, ss));
-    CK(cudaStreamWaitEvent(s, ov->end, 0));
   }
 #undef CK
   if (p0.finalize != 0) {

@@ -125,15 +125,9 @@ size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 // band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
 bool frame5_eligible(const FrameParams& p);
-// Context-owned streams/events that pipeline chunk i's shading with chunk i+1's
-// blur (blurred scratch double-buffered).  null -> everything on the caller's stream.
-struct Overlap {
-  cudaStream_t blur, shade;
-  cudaEvent_t start, blur_done[2], shade_done[2], end;
-};
 // kt (nullable, diagnostics): accumulates the CUDA-event time of each kernel
 // kind [blur, shade, epilogue] in ms (synchronises the stream per launch).
-cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, const Overlap* ov, float* kt = nullptr);
+cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, float* kt = nullptr);
 int frame5_launches(const FrameParams& p, long long n_env);
 int frame5_vpitch(int W, int R4);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,
