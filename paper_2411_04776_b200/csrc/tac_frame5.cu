@@ -180,6 +180,9 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   for (int i = ro; i < R; i += cstep) clamp4(reinterpret_cast<float4*>(inb + i * ip) + cg);
   for (int i = R + BH + ro; i < nrows; i += cstep) clamp4(reinterpret_cast<float4*>(inb + i * ip) + cg);
   const int own_rows = min(BH, H - y0);
+  // band rows past the frame bottom (last band, H % 16 != 0) are clamped
+  // replicas of row H-1: converted for the blur, not counted
+  for (int i = own_rows + ro; i < BH; i += cstep) clamp4(reinterpret_cast<float4*>(inb + (R + i) * ip) + cg);
   for (int i = ro; i < own_rows; i += cstep) {
     float4* e = reinterpret_cast<float4*>(inb + (R + i) * ip) + cg;
     const float4 raw = *e;

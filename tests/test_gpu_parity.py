@@ -592,3 +592,29 @@ class TestSensorObserver:
         # masked reset zeroes one env's LoadState only
         obsr.reset(torch.as_tensor(cam), mask=torch.tensor([True, False, False]))
         assert not obsr.state[0].any() and obsr.state[1].any()
+
+
+class TestBandPathShapes:
+    """The default two-kernel path (tac_frame5.cu) at shapes that exercise its
+    edges: partial last band (H % 16 != 0), a single 16-column chunk (both
+    borders in one chunk), several bands of one row-chunk, the reference's
+    DEFAULT_PYRAMID (radius 15 -> R4 = 16) and an identity level (k = 1)."""
+
+    @pytest.mark.parametrize("hw", [(50, 64), (17, 32), (100, 80), (16, 16), (33, 320)])
+    def test_shapes(self, hw):
+        h, w = hw
+        cfg = small_config(h, w, grid=(3, 4))
+        depth = depth_batch(3, h, w, seed=61)
+        shear, twist = synthetic.loads(3, 62)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        for i in range(3):
+            check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
+
+    @pytest.mark.parametrize("ks", [(5, 11, 21, 31), (1, 5, 11)])
+    def test_kernel_size_pyramids(self, ks):
+        cfg = small_config(48, 64, levels=levels_from_kernel_sizes(ks))
+        depth = depth_batch(4, 48, 64, seed=63)
+        shear, twist = synthetic.loads(4, 64)
+        obs = run_pipeline(cfg, depth, shear, twist)
+        for i in range(4):
+            check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
