@@ -618,3 +618,17 @@ class TestBandPathShapes:
         obs = run_pipeline(cfg, depth, shear, twist)
         for i in range(4):
             check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
+
+    def test_env_chunks_match_single_launch(self, monkeypatch):
+        """TAC_CHUNK splits the envs over several (blur, shade) launch pairs:
+        per-chunk views of every per-env buffer must give the same outputs."""
+        n = 7
+        depth = depth_batch(n, 48, 64, seed=65)
+        shear, twist = synthetic.loads(n, 66)
+        ref = run_pipeline(small_config(48, 64), depth, shear, twist)
+        monkeypatch.setenv("TAC_CHUNK", "3")
+        got = run_pipeline(small_config(48, 64), depth, shear, twist)  # new config -> new context
+        assert torch.equal(got.rgb, ref.rgb)
+        assert torch.equal(got.blurred, ref.blurred)
+        assert torch.equal(got.disp, ref.disp)
+        assert torch.equal(got.summary, ref.summary)
