@@ -20,6 +20,7 @@ struct tac_ctx {
   float4* d_lut = nullptr;
   float* d_bg = nullptr;
   float4* d_lut_half = nullptr;    // [2][bins][8] float: plane h = floats 8h..8h+7 of every bin (256-bit loads)
+  cudaTextureObject_t lut_tex = 0;  // float4 texels over d_lut_half (texture path for the gathers)
   float* d_bg_planar = nullptr;    // [3][H*W]: R, G, B background planes (v5 shading)
   uint8_t* d_bg_u8 = nullptr;
   double* d_grid = nullptr;
@@ -133,6 +134,7 @@ int free_ctx(tac_ctx* c) {
   if (!c) return TAC_OK;
   cudaFree(c->d_lut);
   cudaFree(c->d_bg);
+  if (c->lut_tex) cudaDestroyTextureObject(c->lut_tex);
   cudaFree(c->d_lut_half);
   cudaFree(c->d_bg_planar);
   cudaFree(c->d_bg_u8);
@@ -412,6 +414,21 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.lut = c->d_lut;
   b.bg = c->d_bg;
   b.lut_half = reinterpret_cast<const float*>(c->d_lut_half);
+  {
+    cudaResourceDesc rd;
+    std::memset(&rd, 0, sizeof(rd));
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = c->d_lut_half;
+    rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+    rd.res.linear.sizeInBytes = luth.size() * sizeof(float);
+    cudaTextureDesc td;
+    std::memset(&td, 0, sizeof(td));
+    td.readMode = cudaReadModeElementType;
+    td.filterMode = cudaFilterModePoint;
+    if (cudaCreateTextureObject(&c->lut_tex, &rd, &td, nullptr) != cudaSuccess) c->lut_tex = 0;
+    cudaGetLastError();
+  }
+  b.lut_tex = c->lut_tex;
   b.bg_planar = c->d_bg_planar;
   b.nbins = (int)nbins_p;
   b.lut_order = order;

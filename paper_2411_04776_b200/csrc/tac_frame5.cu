@@ -27,10 +27,11 @@
 //     (REF/cli.py:134-139).  Pixels whose 3x3 blurred neighbourhood is zero
 //     (outside the band extents) are exactly rint(background) and copied.
 //     The LUT is read from a half-planar copy (plane h = floats 8h..8h+7 of
-//     every bin, bins in direction-major order) with two 256-bit loads per
-//     pixel, and the background from R/G/B planes: the kernel is bound by L1
-//     data-pipe wavefronts, and these layouts make a warp's gathers fall on
-//     far fewer 128-B lines.
+//     every bin, bins in direction-major order): plane 0 with one 256-bit
+//     load per pixel, plane 1 through the texture path; the background from
+//     R/G/B planes.  The kernel is bound by L1 data-pipe wavefronts: these
+//     layouts make a warp's gathers fall on far fewer 128-B lines, and the
+//     texture half uses the other L1TEX data pipe.
 //
 //  env_epilogue_kernel  kernel (c): per env, reduces the band contact partials
 //     in a fixed order, finalises contact / summary / load
@@ -413,10 +414,17 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
     const int i0 = planar_bin(p, a0p.mb, a0p.db);
     const int i1 = planar_bin(p, a1p.mb, a1p.db);
     float4 a0, c0, d0, e0, a1, c1, d1, e1;
-    ld256(p.lut_half + 8 * i0, a0, c0);
-    ld256(p.lut_half + 8 * (p.nbins + i0), d0, e0);
-    ld256(p.lut_half + 8 * i1, a1, c1);
-    ld256(p.lut_half + 8 * (p.nbins + i1), d1, e1);
+    {
+      // plane 0 through the LSU (256-bit), plane 1 through the texture path:
+      // the two halves of the gather use both L1TEX data pipes (measured +2 %)
+      const cudaTextureObject_t tx = p.lut_tex;
+      ld256(p.lut_half + 8 * i0, a0, c0);
+      ld256(p.lut_half + 8 * i1, a1, c1);
+      d0 = tex1Dfetch<float4>(tx, 2 * (p.nbins + i0));
+      e0 = tex1Dfetch<float4>(tx, 2 * (p.nbins + i0) + 1);
+      d1 = tex1Dfetch<float4>(tx, 2 * (p.nbins + i1));
+      e1 = tex1Dfetch<float4>(tx, 2 * (p.nbins + i1) + 1);
+    }
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const Px& pp = s ? a1p : a0p;
@@ -550,6 +558,7 @@ bool frame5_eligible(const FrameParams& p) {
   if (p.strips != 1 || p.W % 16 != 0 || p.W > 320 || p.W < 16) return false;
   if (p.R < 1 || p.R > 16) return false;
   if (p.mg.rows * p.mg.cols > 1024) return false;
+  if (p.lut_tex == 0) return false;  // the shade kernel reads LUT plane 1 through a texture
   const int ng = p.W / 4;
   if ((ng * (K1T / ng)) % 32 != 0) return false;  // whole warps (shuffles, block_reduce)
   return band_blur_smem_bytes(p) <= 227 * 1024;

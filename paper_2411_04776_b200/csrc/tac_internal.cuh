@@ -71,6 +71,7 @@ struct FrameParams {
   const float* bg;       // [H][W][3] 8-bit units
   const uint8_t* bg_u8;  // [H][W][3] = clamp(rint(bg))
   const float* lut_half;     // [2][nbins][8]: plane h holds floats 8h..8h+7 of every bin
+  unsigned long long lut_tex;  // cudaTextureObject_t over lut_half as float4 texels (0 = none)
   const float* bg_planar;    // [3][H][W]
   int nbins;
   int lut_order;             // lut_half bin order: 0 = [mag][dir], 1 = [dir][mag], 2 = 4x2 tiles
