@@ -51,7 +51,7 @@ namespace tac {
 namespace {
 
 constexpr int BH = 16;    // band rows
-constexpr int K1T = 320;  // blur threads: 16 rows x 20 chunks of 16 columns
+constexpr int K1T = 320;  // blur threads: 8 row pairs x 40 chunks of 8 columns (W = 320)
 constexpr int K2T = 320;  // shade threads
 
 // ---- row-pair interleaved intermediate ----------------------------------------
