@@ -632,3 +632,22 @@ class TestBandPathShapes:
         assert torch.equal(got.blurred, ref.blurred)
         assert torch.equal(got.disp, ref.disp)
         assert torch.equal(got.summary, ref.summary)
+
+
+class TestDiagnostics:
+    def test_launch_count_and_profile(self):
+        cfg = small_config(48, 64)
+        pipe = TactilePipeline(cfg, DEV)
+        n = 5
+        depth = depth_batch(n, 48, 64, seed=71).to(DEV)
+        shear, twist = synthetic.loads(n, 72)
+        out = pipe.allocate(n)
+        args = pipe.launch_args(depth, torch.as_tensor(shear, device=DEV), torch.as_tensor(twist, device=DEV), out)
+        assert pipe.launches_per_call(n) == 3  # band blur, band shade, per-env epilogue
+        ms = pipe.profile(args, iters=2)
+        assert len(ms) == 3 and all(v > 0 for v in ms)
+        # the profiled calls produce the same frame as a plain call
+        rgb = out.rgb.clone()
+        pipe.launch(args)
+        torch.cuda.synchronize()
+        assert torch.equal(out.rgb, rgb)
