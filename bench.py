@@ -8,7 +8,7 @@ Workload (N=1): BASELINE configs[2] -- 4096 envs of 240x320 synthetic height
 maps (sphere / cylinder / cube edge / Perlin plate, penetration U(0, 1.2 mm)),
 sigma (1,2,4) pyramid, 125x180 random LUT, U[80,160] background, 7x9
 markers with random shear/twist, dots r=3.  One step = one fused
-``tac_pipeline`` launch over all envs.  N>1: every rank runs its own 4096-env
+``tac_pipeline`` call over all envs (band blur, band shade, per-env epilogue).  N>1: every rank runs its own 4096-env
 block (weak scaling; at N=8 that is configs[4]'s 32768 envs) plus the NCCL
 all-gather of the [N, 8] contact summaries once per step.
 
@@ -401,7 +401,7 @@ def run_ours(a, rank, world, local_rank):
                 gbs = kb[name] * n_env / (kms / 1e3) / 1e9
                 kernels[name] = {"ms": kms, "bytes_per_frame": kb[name], "achieved_gbs": gbs, "frac": gbs / peak}
         dom = max(kernels, key=lambda k: kernels[k]["ms"])
-    else:  # one fused kernel (TAC_FRAME=3/4)
+    else:  # one fused kernel (TAC_FRAME=3)
         dom = "frame_kernel (fused)"
         kernels[dom] = {"ms": kern_ms[0], "bytes_per_frame": algorithmic_bytes(cfg),
                         "achieved_gbs": step_gbs, "frac": step_gbs / peak}

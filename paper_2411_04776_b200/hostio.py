@@ -4,7 +4,7 @@ The reference returns host-owned observations (REF/envs.py:654-665) and its
 offline driver reads maps from files (REF/cli.py:274-301), so a drop-in
 caller holds HOST buffers.  ``simulate_host`` streams env chunks through the
 GPU on two CUDA streams: H2D of chunk i+1 and D2H of chunk i-1 overlap the
-fused kernel on chunk i.
+kernels of chunk i.
 """
 
 import torch

@@ -81,7 +81,8 @@ class TactilePipeline:
         contact=False,
         splat=True,
     ) -> Observation:
-        """Run the whole path for every env in one launch.
+        """Run the whole path for every env in one ``tac_pipeline`` call
+        (band blur + band shade kernels and a per-env epilogue).
 
         depth: [N, H, W] float32 on the pipeline's device (a HeightMap batch
         when input_kind == "depth", an IndentationMap batch when
