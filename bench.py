@@ -7,9 +7,9 @@
 Workload (N=1): BASELINE configs[2] -- 4096 envs of 240x320 synthetic height
 maps (sphere / cylinder / cube edge / Perlin plate, penetration U(0, 1.2 mm)),
 sigma (1,2,4) pyramid, 125x180 random LUT, U[80,160] background, 7x9
-markers with random shear/twist, dots r=3.  One step = one fused
-``tac_pipeline`` call over all envs (band blur, band shade, per-env epilogue).  N>1: every rank runs its own 4096-env
-block (weak scaling; at N=8 that is configs[4]'s 32768 envs) plus the NCCL
+markers with random shear/twist, dots r=3.  One step = one ``tac_pipeline``
+call over all envs (band blur, band shade, per-env epilogue launches).  N>1:
+every rank runs its own 4096-env block (weak scaling; at N=8 that is configs[4]'s 32768 envs) plus the NCCL
 all-gather of the [N, 8] contact summaries once per step.
 
 Prints ONE JSON line (rank 0).
