@@ -651,3 +651,38 @@ class TestDiagnostics:
         pipe.launch(args)
         torch.cuda.synchronize()
         assert torch.equal(out.rgb, rgb)
+
+    def test_cuda_graph_capture_replays_the_step(self):
+        """The whole tac_pipeline call (all its launches) can be captured in a
+        CUDA graph and replayed, e.g. inside an RL step graph."""
+        cfg = small_config(48, 64)
+        pipe = TactilePipeline(cfg, DEV)
+        n = 6
+        depth = depth_batch(n, 48, 64, seed=73).to(DEV)
+        shear, twist = synthetic.loads(n, 74)
+        sh = torch.as_tensor(shear, device=DEV)
+        tw = torch.as_tensor(twist, device=DEV)
+        out = pipe.allocate(n)
+        args = pipe.launch_args(depth, sh, tw, out)
+        s = torch.cuda.Stream(DEV)
+        s.wait_stream(torch.cuda.current_stream(DEV))
+        with torch.cuda.stream(s):
+            args = pipe.launch_args(depth, sh, tw, out)  # workspace of the capture stream
+            pipe.launch(args)  # warm-up on the capture stream
+        torch.cuda.current_stream(DEV).wait_stream(s)
+        torch.cuda.synchronize()
+        ref = out.rgb.clone(), out.disp.clone(), out.summary.clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            pipe.launch(args)
+        out.rgb.zero_()
+        out.disp.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.rgb, ref[0]) and torch.equal(out.disp, ref[1]) and torch.equal(out.summary, ref[2])
+        depth2 = depth_batch(n, 48, 64, seed=75).to(DEV)
+        depth.copy_(depth2)  # new inputs in place, same graph
+        g.replay()
+        torch.cuda.synchronize()
+        fresh = run_pipeline(small_config(48, 64), depth2, shear, twist)
+        assert torch.equal(out.rgb, fresh.rgb)
