@@ -189,8 +189,11 @@ int tac_render_markers(const tac_ctx* ctx, const float* disp, uint8_t* rgb,
 int tac_shadow(const tac_ctx* ctx, const float* in, int32_t input_kind, float* factor,
                float* rgb, int64_t n_env, void* stream);
 
-/* The fused path: one launch per call.  depth -> rgb (with dots), disp,
- * summary (+ optional blurred) for every env.  Equivalent to, per env:
+/* The whole path in one call (on aligned frames of <= 320 columns: a band
+ * blur kernel, a band shade kernel and a per-env epilogue, see
+ * tac_pipeline_launches; otherwise one fused kernel).  depth -> rgb (with
+ * dots), disp, summary (+ optional blurred) for every env.  No host
+ * synchronisation, no allocation: CUDA-graph capturable.  Equivalent to, per env:
  * indentation_from -> smooth_pyramid -> shade -> uint8 ; contact_center ->
  * (given load | track_load) -> marker_displacements -> render_markers. */
 typedef struct tac_pipeline_args {
