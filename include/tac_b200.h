@@ -150,6 +150,12 @@ int tac_normals(const tac_ctx* ctx, const float* elev, float* normals,
  * rule of REF/cli.py:134-139).  blurred [N,H,W] -> rgb [N,H,W,3] uint8. */
 int tac_shade(const tac_ctx* ctx, const float* blurred, uint8_t* rgb,
               int64_t n_env, void* stream);
+/* tac_shade plus, per env, the number of channel values the [0, 255] clip
+ * changed (the reference's `raw != clip(raw)` count behind its >1 %
+ * saturation warning, REF/optical.py:246-249).  saturated: uint32 [N] (zeroed
+ * here), nullable. */
+int tac_shade_ex(const tac_ctx* ctx, const float* blurred, uint8_t* rgb, uint32_t* saturated,
+                 int64_t n_env, void* stream);
 
 /* contact_center (REF/marker.py:103-121) on the raw (unsmoothed) map.
  * contact (nullable): fp64 [N,8] LoadState layout (below) with shear/twist 0,

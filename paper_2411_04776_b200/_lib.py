@@ -100,6 +100,7 @@ SIGNATURES = {
     "tac_contact_blur": (ctypes.c_int, [_p, _p, _i32, _p, _p, _p, _i64, _p]),
     "tac_normals": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
     "tac_shade": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
+    "tac_shade_ex": (ctypes.c_int, [_p, _p, _p, _p, _i64, _p]),
     "tac_contact": (ctypes.c_int, [_p, _p, _i32, _p, _p, _p, _i64, _p]),
     "tac_track_load": (ctypes.c_int, [_p, _p, _p, _p, _i64, _p]),
     "tac_marker_displacements": (ctypes.c_int, [_p, _p, _p, _i64, _p]),

@@ -529,14 +529,19 @@ int tac_normals(const tac_ctx* c, const float* elev, float* normals, int64_t n_e
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_normals");
 }
 
-int tac_shade(const tac_ctx* c, const float* blurred, uint8_t* rgb, int64_t n_env, void* stream) {
+int tac_shade_ex(const tac_ctx* c, const float* blurred, uint8_t* rgb, uint32_t* saturated, int64_t n_env,
+                 void* stream) {
   int st = common_checks(c, n_env);
   if (st) return st;
   if (n_env && (!blurred || !rgb)) return fail(TAC_ERR_INVALID, "null buffer");
   FrameParams p = c->fused;
   p.n_env = n_env;
-  cudaError_t e = launch_shade(p, blurred, rgb, n_env, (cudaStream_t)stream);
+  cudaError_t e = launch_shade(p, blurred, rgb, saturated, n_env, (cudaStream_t)stream);
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_shade");
+}
+
+int tac_shade(const tac_ctx* c, const float* blurred, uint8_t* rgb, int64_t n_env, void* stream) {
+  return tac_shade_ex(c, blurred, rgb, nullptr, n_env, stream);
 }
 
 int tac_contact(const tac_ctx* c, const float* in, int32_t input_kind, double* contact,

@@ -761,7 +761,8 @@ cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s) {
 // Stand-alone shade (kernel (b) from a blurred map in HBM), one pixel per thread.
 __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ FrameParams p,
                                                     const float* __restrict__ blurred,
-                                                    uint8_t* __restrict__ rgb) {
+                                                    uint8_t* __restrict__ rgb,
+                                                    unsigned int* __restrict__ saturated) {
   const long long HW = (long long)p.H * p.W;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= p.n_env * HW) return;
@@ -778,17 +779,25 @@ __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ Fram
   const float* bgp = p.bg + (long long)pix * 3;
   float r = bgp[0], g = bgp[1], bl = bgp[2];
   shade_one(p, gx, gy, r, g, bl);
+  if (saturated) {  // channel values the clip changes: REF/optical.py:246-247 (raw != out)
+    const unsigned c = (r < 0.f || r > 255.f) + (g < 0.f || g > 255.f) + (bl < 0.f || bl > 255.f);
+    if (c) atomicAdd(saturated + env, c);
+  }
   uint8_t* d = rgb + i * 3;
   d[0] = (uint8_t)u8sat(r);
   d[1] = (uint8_t)u8sat(g);
   d[2] = (uint8_t)u8sat(bl);
 }
 
-cudaError_t launch_shade(const FrameParams& p, const float* blurred, uint8_t* rgb, long long n_env,
-                         cudaStream_t s) {
+cudaError_t launch_shade(const FrameParams& p, const float* blurred, uint8_t* rgb, unsigned int* saturated,
+                         long long n_env, cudaStream_t s) {
   const long long n = n_env * (long long)p.H * p.W;
   if (n == 0) return cudaSuccess;
-  shade_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, blurred, rgb);
+  if (saturated) {
+    cudaError_t e = cudaMemsetAsync(saturated, 0, sizeof(unsigned int) * n_env, s);
+    if (e != cudaSuccess) return e;
+  }
+  shade_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, blurred, rgb, saturated);
   return cudaGetLastError();
 }
 

@@ -135,7 +135,7 @@ cudaError_t launch_indentation(const float* depth, float* ind, float rest, float
                                cudaStream_t s);
 cudaError_t launch_normals(const float* elev, float* normals, int H, int W, float inv_p,
                            float inv_2p, long long n_env, cudaStream_t s);
-cudaError_t launch_shade(const FrameParams& p, const float* blurred, uint8_t* rgb,
+cudaError_t launch_shade(const FrameParams& p, const float* blurred, uint8_t* rgb, unsigned int* saturated,
                          long long n_env, cudaStream_t s);
 cudaError_t launch_track_load(double* state, const double* pose_delta, const double* contact,
                               long long n_env, cudaStream_t s);

@@ -5,6 +5,8 @@ binned 125x180 LUT of the north star.  The reference's global
 polynomial ``PolyTable`` is the single-bin special case (``lut_from_polytable``).
 """
 
+import logging
+
 import numpy as np
 import torch
 
@@ -42,12 +44,19 @@ def normals_from(source, pixel_pitch=None) -> torch.Tensor:
     return out[0] if single else out
 
 
-def shade(smoothed, cfg: PipelineConfig) -> torch.Tensor:
+log = logging.getLogger(__name__)
+_SATURATION_WARN_FRACTION = 0.01  # REF/optical.py:29
+
+
+def shade(smoothed, cfg: PipelineConfig, *, warn_saturation: bool = True) -> torch.Tensor:
     """Kernel (b): smoothed indentation [N, H, W] -> uint8 RGB [N, H, W, 3].
 
     gradient (REF/optical.py:160) -> bins -> per-bin quadratic in (nx, ny)
     (basis REF/optical.py:82-88, c0 cancels as REF/optical.py:244) -> + bg ->
-    rint -> clamp (uint8 rule REF/cli.py:134-139)."""
+    rint -> clamp (uint8 rule REF/cli.py:134-139).  Like the reference, logs a
+    warning for a frame whose clip changed more than 1 % of the channel values
+    (REF/optical.py:246-249); that check reads a per-env count back from the
+    device (``warn_saturation=False`` skips it)."""
     v = smoothed.values if isinstance(smoothed, IndentationMap) else smoothed
     single = v.dim() == 2
     v = (v.unsqueeze(0) if single else v).contiguous()
@@ -55,7 +64,13 @@ def shade(smoothed, cfg: PipelineConfig) -> torch.Tensor:
     n = v.shape[0]
     require(v, "smoothed", torch.float32, (n, ctx.H, ctx.W), ctx.device)
     out = torch.empty((n, ctx.H, ctx.W, 3), dtype=torch.uint8, device=v.device)
-    _lib.check(ctx.lib.tac_shade(ctx.handle, v.data_ptr(), out.data_ptr(), n, ctx.stream()), "tac_shade")
+    sat = torch.empty((n,), dtype=torch.int32, device=v.device) if warn_saturation and n else None
+    _lib.check(ctx.lib.tac_shade_ex(ctx.handle, v.data_ptr(), out.data_ptr(),
+                                    sat.data_ptr() if sat is not None else None, n, ctx.stream()), "tac_shade")
+    if sat is not None:
+        frac = sat.double().cpu() / (3.0 * ctx.H * ctx.W)
+        for i in torch.nonzero(frac > _SATURATION_WARN_FRACTION).flatten().tolist():
+            log.warning("shade: %.1f%% of pixels saturated (env %d)", 100.0 * float(frac[i]), i)
     return out[0] if single else out
 
 

@@ -286,6 +286,36 @@ class TestMirrorsAgainstReferenceGolden:
         mx, frac = rgb_stats(rgb, g["shaded_u8"])
         assert mx <= 1 and frac >= RGB_FRAC
 
+    def test_saturation_warning(self, caplog):
+        """REF tests/test_optical.py:173-184: a table whose nx term drives the
+        shading far outside [0, 1] logs the saturation warning; the count
+        behind it is every channel of every pixel here."""
+        import logging
+
+        from paper_2411_04776_b200 import lut_from_polytable
+
+        h, w, pitch = 20, 32, 2.66e-5
+        coeffs = np.zeros((3, 6))
+        coeffs[:, 0] = 0.9
+        coeffs[:, 1] = 5.0
+        cfg = PipelineConfig(
+            sensor=SensorConfig.from_pitch(h, w, pitch, 4e-3, (3, 3)),
+            levels=levels_from_kernel_sizes(),
+            lut=lut_from_polytable(coeffs),
+            background=np.full((h, w, 3), 0.9 * 255.0, np.float32),
+        )
+        ramp = torch.arange(w, dtype=torch.float32, device=DEV) * (0.577 * pitch)
+        sm = torch.stack([ramp.expand(h, w), torch.zeros(h, w, device=DEV)]).contiguous()
+        with caplog.at_level(logging.WARNING, logger="paper_2411_04776_b200.optical"):
+            rgb = shade(sm, cfg)
+        msgs = [r.message for r in caplog.records if "saturated" in r.message]
+        assert len(msgs) == 1 and "100.0%" in msgs[0] and "env 0" in msgs[0]  # flat env 1 is silent
+        assert (rgb[1] == round(0.9 * 255.0)).all()
+        caplog.clear()
+        with caplog.at_level(logging.WARNING, logger="paper_2411_04776_b200.optical"):
+            shade(sm, cfg, warn_saturation=False)
+        assert not caplog.records
+
     def test_contact_center(self, golden):
         g = golden("marker")
         sensor = SensorConfig.from_pitch(48, 64, 2.66e-5, 4e-3, (7, 9))
