@@ -664,6 +664,27 @@ class TestBandPathShapes:
         assert torch.equal(got.summary, ref.summary)
 
 
+    def test_host_streamer_matches_device_call(self):
+        """The e2e path bench.py times (pinned host buffers, two streams, H2D /
+        kernels / D2H per env chunk, ragged last chunk) returns exactly what
+        one device-resident call returns."""
+        from paper_2411_04776_b200.hostio import simulate_host
+
+        cfg = small_config(48, 64)
+        n = 11
+        depth = depth_batch(n, 48, 64, seed=67)
+        shear, twist = synthetic.loads(n, 68)
+        pipe = TactilePipeline(cfg, DEV)
+        sh = torch.as_tensor(shear, dtype=torch.float64)
+        tw = torch.as_tensor(twist, dtype=torch.float64)
+        ref = pipe.simulate(depth.to(DEV), sh.to(DEV), tw.to(DEV))
+        torch.cuda.synchronize()
+        got = simulate_host(pipe, depth.pin_memory(), sh.pin_memory(), tw.pin_memory(), chunk=4)
+        assert not got.rgb.is_cuda
+        assert torch.equal(got.rgb, ref.rgb.cpu())
+        assert torch.equal(got.disp, ref.disp.cpu())
+        assert torch.equal(got.summary, ref.summary.cpu())
+
 class TestDiagnostics:
     def test_launch_count_and_profile(self):
         cfg = small_config(48, 64)
