@@ -475,14 +475,6 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   const int2 e1 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
   const int sa = min(e0.x, e1.x), sb = max(e0.y, e1.y);
   // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
-#ifdef TAC_K2_SPEC
-  // blurred rows loaded unconditionally, in parallel with the extent loads
-  // (the blurred scratch is written everywhere, zeros included)
-  float4 cc = *reinterpret_cast<const float4*>(rc);
-  float4 mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
-  float4 nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
-  const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
-#else
   const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
   float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
   if (any) {
@@ -490,7 +482,6 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
     mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
     nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
   }
-#endif
   float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
   float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
   bool done = false;
