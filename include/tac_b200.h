@@ -118,6 +118,15 @@ int32_t tac_pipeline_launches(const tac_ctx* ctx, int64_t n_env);
  * fused frame kernel), [1] = shade, [2] = per-env epilogue (0 when absent). */
 int tac_pipeline_profile(const tac_ctx* ctx, const struct tac_pipeline_args* args, void* stream,
                          int32_t iters, float* kernel_ms);
+/* Diagnostics: between tac_timing_begin and tac_timing_end, the first
+ * max_calls single-chunk band-path tac_pipeline calls on this context record
+ * CUDA events at their kernel boundaries on the call's stream (no
+ * synchronisation, so a timed loop runs unchanged).  tac_timing_end waits for
+ * the last event and writes the mean per-call milliseconds of [blur, shade,
+ * epilogue] and the number of calls recorded (0: none; e.g. the fused path).
+ * Not thread-safe while timing is on. */
+int tac_timing_begin(const tac_ctx* ctx, int32_t max_calls);
+int tac_timing_end(const tac_ctx* ctx, float* kernel_ms, int32_t* calls);
 
 /* render_heightmap (REF/tactile.py:129-190): orthographic z-buffer of
  * camera-frame triangles.  verts: fp64 [N][n_verts][3] (camera frame, one

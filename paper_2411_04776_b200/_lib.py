@@ -95,6 +95,8 @@ SIGNATURES = {
     "tac_tiles_per_frame": (_i32, [_p]),
     "tac_pipeline_launches": (_i32, [_p, _i64]),
     "tac_pipeline_profile": (ctypes.c_int, [_p, ctypes.POINTER(TacPipelineArgs), _p, _i32, _p]),
+    "tac_timing_begin": (ctypes.c_int, [_p, _i32]),
+    "tac_timing_end": (ctypes.c_int, [_p, _p, _p]),
     "tac_render_heightmap": (ctypes.c_int, [_p, _p, _i64, _p, _i64, _p, _i64, _p]),
     "tac_indentation": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
     "tac_contact_blur": (ctypes.c_int, [_p, _p, _i32, _p, _p, _p, _i64, _p]),

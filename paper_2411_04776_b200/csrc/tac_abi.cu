@@ -33,6 +33,13 @@ struct tac_ctx {
   long long chunk5;                  // envs per v5 launch pair
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
+  // diagnostics: boundary events of the pipeline calls between
+  // tac_timing_begin and tac_timing_end (not thread-safe while on)
+  mutable struct {
+    std::vector<cudaEvent_t> ev;
+    int cap = 0, used = 0;
+    bool on = false;
+  } timing;
 };
 
 namespace {
@@ -141,6 +148,7 @@ int free_ctx(tac_ctx* c) {
   cudaFree(c->d_grid);
   cudaFree(c->d_shadow_off);
   cudaFree(c->d_shadow_cost);
+  for (cudaEvent_t e : c->timing.ev) cudaEventDestroy(e);
   delete c;
   return TAC_OK;
 }
@@ -644,7 +652,11 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
   cudaError_t e;
   if (v5) {
     bind_workspace5(c, p, a->workspace, a->n_env);
-    e = launch_frame5(p, (cudaStream_t)stream, kt);
+    cudaEvent_t* ev4 = nullptr;
+    auto& tg = c->timing;
+    if (tg.on && !kt && tg.used < tg.cap && (c->chunk5 <= 0 || a->n_env <= c->chunk5))
+      ev4 = tg.ev.data() + 4 * tg.used++;
+    e = launch_frame5(p, (cudaStream_t)stream, kt, ev4);
   } else {
     bind_workspace(c, p, a->workspace, a->n_env);
     cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -680,6 +692,46 @@ int32_t tac_pipeline_launches(const tac_ctx* c, int64_t n_env) {
     return frame5_launches(p, n_env);
   }
   return n_env > 0 ? 1 : 0;
+}
+
+int tac_timing_begin(const tac_ctx* c, int32_t max_calls) {
+  if (!c) return fail(TAC_ERR_INVALID, "null context");
+  if (max_calls < 1) return fail(TAC_ERR_INVALID, "max_calls must be >= 1");
+  int st = check_device(c);
+  if (st) return st;
+  auto& tg = c->timing;
+  while ((int)tg.ev.size() < 4 * max_calls) {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) return cuda_fail(r, "cudaEventCreate");
+    tg.ev.push_back(e);
+  }
+  tg.cap = max_calls;
+  tg.used = 0;
+  tg.on = true;
+  return TAC_OK;
+}
+
+int tac_timing_end(const tac_ctx* c, float* kernel_ms, int32_t* calls) {
+  if (!c || !kernel_ms || !calls) return fail(TAC_ERR_INVALID, "null argument");
+  auto& tg = c->timing;
+  tg.on = false;
+  for (int k = 0; k < 3; ++k) kernel_ms[k] = 0.f;
+  *calls = tg.used;
+  if (tg.used == 0) return TAC_OK;
+  cudaError_t r = cudaEventSynchronize(tg.ev[4 * tg.used - 1]);
+  if (r != cudaSuccess) return cuda_fail(r, "cudaEventSynchronize");
+  double sum[3] = {0, 0, 0};
+  for (int i = 0; i < tg.used; ++i)
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      r = cudaEventElapsedTime(&ms, tg.ev[4 * i + k], tg.ev[4 * i + k + 1]);
+      if (r != cudaSuccess) return cuda_fail(r, "cudaEventElapsedTime");
+      sum[k] += ms;
+    }
+  for (int k = 0; k < 3; ++k) kernel_ms[k] = (float)(sum[k] / tg.used);
+  tg.used = 0;  // reported once
+  return TAC_OK;
 }
 
 int tac_pipeline_profile(const tac_ctx* c, const tac_pipeline_args* a, void* stream, int32_t iters,

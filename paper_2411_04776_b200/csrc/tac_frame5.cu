@@ -168,10 +168,14 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
   auto clamp4 = [&](float4* e) -> float4 {
     float4 v = *e;
     if (p.input_depth) {
-      v.x = clampf((p.rest - v.x) + p.rest_lo, 0.f, p.rest);
-      v.y = clampf((p.rest - v.y) + p.rest_lo, 0.f, p.rest);
-      v.z = clampf((p.rest - v.z) + p.rest_lo, 0.f, p.rest);
-      v.w = clampf((p.rest - v.w) + p.rest_lo, 0.f, p.rest);
+      // (rest - depth) + rest_lo in pairs (FADD2), each step rounded as the scalar form
+      const float2 rr = make_float2(p.rest, p.rest), rl = make_float2(p.rest_lo, p.rest_lo);
+      const float2 a = fsubadd2(rr, make_float2(v.x, v.y), rl);
+      const float2 b = fsubadd2(rr, make_float2(v.z, v.w), rl);
+      v.x = clampf(a.x, 0.f, p.rest);
+      v.y = clampf(a.y, 0.f, p.rest);
+      v.z = clampf(b.x, 0.f, p.rest);
+      v.w = clampf(b.y, 0.f, p.rest);
       *e = v;
     }
     // any non-zero bit pattern (a -0 only widens the extent: still exact)
@@ -589,7 +593,7 @@ struct KTimer {
   }
 };
 
-cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt) {
+cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt, cudaEvent_t* ev4) {
   const size_t smem = band_blur_smem_bytes(p0);
   cudaError_t e = cudaFuncSetAttribute(band_blur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -603,6 +607,10 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt) {
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
   const long long nchunks = (p0.n_env + chunk - 1) / chunk;
   KTimer tm(kt, s);
+  // in-stream boundary events (no synchronisation): before blur, after blur,
+  // after shade, after the epilogue; single-chunk calls only
+  if (nchunks != 1) ev4 = nullptr;
+  if (ev4) cudaEventRecord(ev4[0], s);
 #define CK(x)                          \
   do {                                 \
     e = (x);                           \
@@ -623,10 +631,12 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt) {
     band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
     CK(cudaGetLastError());
     tm.stop(0);
+    if (ev4) cudaEventRecord(ev4[1], s);
     tm.start();
     band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
     CK(cudaGetLastError());
     tm.stop(1);
+    if (ev4) cudaEventRecord(ev4[2], s);
   }
 #undef CK
   if (p0.finalize != 0) {
@@ -635,6 +645,7 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt) {
     e = cudaGetLastError();
     tm.stop(2);
   }
+  if (ev4) cudaEventRecord(ev4[3], s);
   return e;
 }
 

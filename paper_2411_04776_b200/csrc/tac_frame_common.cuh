@@ -117,6 +117,16 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return r;
 }
 
+// Paired fp32 (a - b) + c, each step rounded (FADD2 x2 on sm_100a).
+__device__ __forceinline__ float2 fsubadd2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n sub.rn.f32x2 rd, ra, rb;\n add.rn.f32x2 rd, rd, rc;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
 // ---- shading ------------------------------------------------------------------
 // atan(a) for a in [0, 1]: odd minimax polynomial, |err| ~ 1e-7 rad in fp32.
 __device__ __forceinline__ float atan01(float a) {

@@ -128,7 +128,7 @@ cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 bool frame5_eligible(const FrameParams& p);
 // kt (nullable, diagnostics): accumulates the CUDA-event time of each kernel
 // kind [blur, shade, epilogue] in ms (synchronises the stream per launch).
-cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, float* kt = nullptr);
+cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, float* kt = nullptr, cudaEvent_t* ev4 = nullptr);
 int frame5_launches(const FrameParams& p, long long n_env);
 int frame5_vpitch(int W, int R4);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,

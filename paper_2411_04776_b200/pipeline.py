@@ -175,5 +175,17 @@ class TactilePipeline:
                                                      int(iters), ms), "tac_pipeline_profile")
         return [float(v) for v in ms]
 
+    def timing_begin(self, max_calls):
+        """Record kernel-boundary CUDA events in the next ``max_calls`` pipeline
+        calls (diagnostics; no synchronisation inside the calls)."""
+        _lib.check(self.ctx.lib.tac_timing_begin(self.ctx.handle, int(max_calls)), "tac_timing_begin")
+
+    def timing_end(self):
+        """(mean per-call ms of [blur, shade, epilogue], calls recorded)."""
+        ms = (ctypes.c_float * 3)()
+        calls = ctypes.c_int32(0)
+        _lib.check(self.ctx.lib.tac_timing_end(self.ctx.handle, ms, ctypes.byref(calls)), "tac_timing_end")
+        return [float(v) for v in ms], int(calls.value)
+
 
 __all__ = ["TactilePipeline", "Observation", "SUMMARY_FIELDS", "_ptr"]

@@ -117,6 +117,8 @@ def test_null_context_calls_fail_cleanly():
     assert lib.tac_pipeline(None, None, None) == _lib.TAC_ERR_INVALID
     assert lib.tac_shade(None, None, None, 0, None) == _lib.TAC_ERR_INVALID
     assert lib.tac_shade_ex(None, None, None, None, 0, None) == _lib.TAC_ERR_INVALID
+    assert lib.tac_timing_begin(None, 4) == _lib.TAC_ERR_INVALID
+    assert lib.tac_timing_end(None, None, None) == _lib.TAC_ERR_INVALID
     assert lib.tac_render_heightmap(None, None, 0, None, 0, None, 1, None) == _lib.TAC_ERR_INVALID
     assert lib.tac_pipeline_profile(None, None, None, 1, None) == _lib.TAC_ERR_INVALID
     assert lib.tac_pipeline_launches(None, 10) == 0

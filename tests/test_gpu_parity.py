@@ -703,6 +703,29 @@ class TestDiagnostics:
         torch.cuda.synchronize()
         assert torch.equal(out.rgb, rgb)
 
+    def test_in_stream_kernel_timing(self):
+        """tac_timing_begin/end: boundary events of the next calls, no
+        synchronisation inside them; outputs unchanged; capped at max_calls."""
+        cfg = small_config(48, 64)
+        pipe = TactilePipeline(cfg, DEV)
+        n = 5
+        depth = depth_batch(n, 48, 64, seed=75).to(DEV)
+        shear, twist = synthetic.loads(n, 76)
+        out = pipe.allocate(n)
+        args = pipe.launch_args(depth, torch.as_tensor(shear, device=DEV), torch.as_tensor(twist, device=DEV), out)
+        pipe.launch(args)
+        torch.cuda.synchronize()
+        rgb = out.rgb.clone()
+        pipe.timing_begin(3)
+        for _ in range(4):
+            pipe.launch(args)
+        ms, calls = pipe.timing_end()
+        assert calls == 3 and len(ms) == 3 and all(v > 0 for v in ms)
+        torch.cuda.synchronize()
+        assert torch.equal(out.rgb, rgb)
+        ms, calls = pipe.timing_end()  # nothing recorded since
+        assert calls == 0 and ms == [0.0, 0.0, 0.0]
+
     def test_cuda_graph_capture_replays_the_step(self):
         """The whole tac_pipeline call (all its launches) can be captured in a
         CUDA graph and replayed, e.g. inside an RL step graph."""
