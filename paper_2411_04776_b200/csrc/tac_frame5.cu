@@ -21,7 +21,7 @@
 //     replicate pads of the first/last chunk are written by the thread that
 //     reads them.  Interior bands load their 16 + 2R rows with one bulk copy.
 //
-//  band_shade_kernel  kernel (b): 4 pixels per thread, ~40 warps per SM.
+//  band_shade_kernel  kernel (b): 4 pixels per thread, 160-thread CTAs (whole warps), ~40 warps per SM.
 //     np.gradient differences (REF/optical.py:160), bins, binned-LUT
 //     shading (REF/optical.py:82-88, :244) + background, uint8 rule
 //     (REF/cli.py:134-139).  Pixels whose 3x3 blurred neighbourhood is zero
@@ -52,7 +52,8 @@ namespace {
 
 constexpr int BH = 16;    // band rows
 constexpr int K1T = 320;  // blur threads: 8 row pairs x 40 chunks of 8 columns (W = 320)
-constexpr int K2T = 320;  // shade threads
+constexpr int K2T = 320;     // shade threads per CTA, at most
+constexpr int K2_MIN = 160;  // preferred smallest shade CTA (measured: 160 > 320 > 640 threads at W = 320)
 
 // ---- row-pair interleaved intermediate ----------------------------------------
 // vb2[m][col] = (V[2m][col], V[2m+1][col]) as float2: the horizontal FFMA2
@@ -549,6 +550,17 @@ size_t band_blur_smem_bytes(const FrameParams& p) {
   return sizeof(float) * ((size_t)(BH + 2 * p.R) * p.in_pitch + (size_t)BH * p.v_pitch);
 }
 
+// Rows per shade CTA: whole warps (the row-neighbour shuffles), the smallest
+// such CTA of at least K2_MIN threads, at most K2T; 0 if none.
+int shade_rows_per_cta(int ng) {
+  int r0 = 1;
+  while ((ng * r0) % 32 != 0) ++r0;
+  if (ng * r0 > K2T) return 0;
+  int r = r0;
+  while (ng * r < K2_MIN && ng * (r + r0) <= K2T) r += r0;
+  return r;
+}
+
 bool frame5_eligible(const FrameParams& p) {
   if (p.strips != 1 || p.W % 16 != 0 || p.W > 320 || p.W < 16) return false;
   if (p.R < 1 || p.R > 16) return false;
@@ -556,6 +568,7 @@ bool frame5_eligible(const FrameParams& p) {
   if (p.lut_tex == 0) return false;  // the shade kernel reads LUT plane 1 through a texture
   const int ng = p.W / 4;
   if ((ng * (K1T / ng)) % 32 != 0) return false;  // whole warps (shuffles, block_reduce)
+  if (shade_rows_per_cta(ng) == 0) return false;
   return band_blur_smem_bytes(p) <= 227 * 1024;
 }
 
@@ -601,7 +614,7 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt, cuda
   const long long HW = (long long)p0.H * p0.W;
   const int ng = p0.W / 4;
   const dim3 b1(ng, K1T / ng);
-  const int rpc = K2T / ng;
+  const int rpc = shade_rows_per_cta(ng);
   const dim3 b2(ng, rpc);
   const unsigned nq = (unsigned)((p0.H + rpc - 1) / rpc);
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;

@@ -630,7 +630,10 @@ class TestBandPathShapes:
     borders in one chunk), several bands of one row-chunk, the reference's
     DEFAULT_PYRAMID (radius 15 -> R4 = 16) and an identity level (k = 1)."""
 
-    @pytest.mark.parametrize("hw", [(50, 64), (17, 32), (100, 80), (16, 16), (33, 320)])
+    # (20, 256) / (24, 144): 3- and 8-row shade CTAs; (18, 240): no whole-warp
+    # shade CTA -> the fused-kernel fallback
+    @pytest.mark.parametrize("hw", [(50, 64), (17, 32), (100, 80), (16, 16), (33, 320), (20, 256), (24, 144),
+                                    (18, 240)])
     def test_shapes(self, hw):
         h, w = hw
         cfg = small_config(h, w, grid=(3, 4))
