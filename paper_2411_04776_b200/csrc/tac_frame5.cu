@@ -313,7 +313,9 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
             break;
         }
       }
-      __syncthreads();
+      // the next level's V pass overwrites vb (no barrier after the last level:
+      // only registers and HBM are touched from here on)
+      if (l + 1 < p.n_levels) __syncthreads();
     }
   }
   // ---- blurred band out (exact zeros outside [ha, hb]) --------------------------
