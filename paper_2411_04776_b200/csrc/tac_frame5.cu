@@ -141,9 +141,8 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_lo = INT_MAX;
     s_hi = INT_MIN;
-  }
-  __syncthreads();
-  if (tid == 0) {
+    // the copies are issued before the CTA barrier that publishes the
+    // initialised mbarrier to the waiting threads
     mbar_expect_tx(&s_bar, row_bytes * (unsigned)nrows);
     if (y0 - R >= 0 && y0 + BH + R <= H && ip == W) {
       // interior band: the 16 + 2R rows are one contiguous block
@@ -155,6 +154,7 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
       }
     }
   }
+  __syncthreads();
 
   // ---- conversion: float4 groups, thread -> fixed column group ----------------
   // rows [0, R) and [R + BH, nrows) are halo (clamp + extent only); rows
