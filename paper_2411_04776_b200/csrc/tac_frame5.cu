@@ -517,11 +517,14 @@ __global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant
   __shared__ int s_int[2 * 1024];
   const long long env = blockIdx.x;
   const int nb = p.bands;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp 0: lane s folds bands s, s + 32, ...; then a fixed xor butterfly
+    // (every lane ends with the same bits: deterministic for a given band count)
+    const int lane = threadIdx.x;
     double cnt = 0, sw = 0, swx = 0, swy = 0, nf = 0;
     float mx = 0.f;
     const double* q = p.partials + env * nb * kSumFields;
-    for (int s = 0; s < nb; ++s) {
+    for (int s = lane; s < nb; s += 32) {
       cnt += q[s * 8 + 0];
       sw += q[s * 8 + 1];
       swx += q[s * 8 + 2];
@@ -529,7 +532,16 @@ __global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant
       mx = fmaxf(mx, (float)q[s * 8 + 4]);
       nf += q[s * 8 + 5];
     }
-    finalize_load(p, env, cnt, sw, swx, swy, mx, nf, s_dbl);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      sw += __shfl_xor_sync(0xffffffffu, sw, o);
+      swx += __shfl_xor_sync(0xffffffffu, swx, o);
+      swy += __shfl_xor_sync(0xffffffffu, swy, o);
+      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) finalize_load(p, env, cnt, sw, swx, swy, mx, nf, s_dbl);
   }
   __syncthreads();
   if (p.finalize != 2) return;
