@@ -17,12 +17,16 @@
  *     only enqueues work; nothing synchronises the host.
  *   - The caller owns every buffer.  The library never allocates per call.
  *     Calls that reduce over a frame take a `workspace` of
- *     tac_workspace_bytes(ctx, n_env) bytes that must be ZERO-FILLED ONCE when
- *     allocated; the kernels leave it zeroed again on exit, so a workspace can
- *     be reused by later calls on the same stream.  Use one workspace per
- *     concurrently running stream.
+ *     tac_workspace_bytes(ctx, n_env) bytes (device memory, contents
+ *     irrelevant: every call initialises what it uses on its own stream, so
+ *     a workspace can be reused by later calls of any size).  Calls running
+ *     concurrently need distinct workspaces.
  *   - A context is immutable after creation: calls are reentrant across
- *     host threads and streams.
+ *     host threads and streams.  The only exception is the diagnostics pair
+ *     tac_timing_begin / tac_timing_end (one timing session per context).
+ *   - Structs passed by pointer start with `struct_size` = sizeof(struct);
+ *     a mismatch returns TAC_ERR_INVALID instead of reading past the
+ *     caller's struct.
  *   - Return value: TAC_OK or an error status; tac_last_error() returns a
  *     thread-local message for the last failing call on this thread.  The
  *     error classes mirror REF/errors.py:6-11 (InvalidArgumentError).
@@ -38,6 +42,7 @@
 extern "C" {
 #endif
 
+#define TAC_ABI_VERSION 2
 #define TAC_MAX_LEVELS 8
 #define TAC_MAX_RADIUS 24
 #define TAC_MAX_LIGHTS 4
@@ -56,6 +61,21 @@ enum {
   TAC_INPUT_INDENTATION = 1  /* IndentationMap values: penetration >= 0 (REF/tactile.py:90-107) */
 };
 
+/* LUT storage precision (tac_config.lut_dtype).  F32 is exact; F16 halves
+ * the shade kernel's gather bytes (15 coefficients in one 32-B sector per
+ * bin) at <= 2^-11 relative error per coefficient. */
+enum {
+  TAC_LUT_F32 = 0,
+  TAC_LUT_F16 = 1
+};
+
+/* Kernel selection for tac_pipeline (tac_config.kernel_path). */
+enum {
+  TAC_PATH_AUTO = 0,  /* fastest eligible path (see tac_pipeline_path) */
+  TAC_PATH_BAND = 1,  /* round-1 band-tiled blur + band shade (W <= 320, R <= 16) */
+  TAC_PATH_FUSED = 2  /* strip-streaming fused frame kernel (any shape) */
+};
+
 /* Load sources for the marker stage of tac_pipeline. */
 enum {
   TAC_LOAD_GIVEN = 0, /* shear[N,2] (m) and twist[N] (rad) supplied per env */
@@ -70,6 +90,8 @@ enum {
  * render_markers REF/marker.py:203-234.
  */
 typedef struct tac_config {
+  uint32_t struct_size;     /* = sizeof(tac_config); tac_ctx_create rejects any other
+                               value (a caller built against a different header) */
   int32_t height, width;    /* image_size (H, W); both >= 2 */
   double pixel_pitch;       /* m per pixel (square pixels) */
   double gel_thickness;     /* rest surface depth, m */
@@ -97,26 +119,35 @@ typedef struct tac_config {
   double shadow_factor;                      /* in [0, 1] */
   int32_t shadow_steps;                      /* max_steps, 1..TAC_MAX_SHADOW_STEPS */
   double shadow_softness;                    /* soft-edge width, m, > 0 */
+
+  /* Execution choices (0 = library default).  They change speed, never the
+   * arithmetic, except lut_dtype (see TAC_LUT_*). */
+  int32_t lut_dtype;                         /* TAC_LUT_* */
+  int32_t kernel_path;                       /* TAC_PATH_* */
+  int32_t chunk_envs;                        /* envs per blur/shade launch pair; 0 = 4096 */
 } tac_config;
 
 typedef struct tac_ctx tac_ctx;
+typedef struct tac_pipeline_args tac_pipeline_args; /* defined with tac_pipeline below */
 
 /* Build a context: validates `cfg`, uploads the LUT (repacked), background,
  * quantised background, Gaussian taps and marker grid to the current device. */
 int tac_ctx_create(const tac_config* cfg, tac_ctx** out);
 int tac_ctx_destroy(tac_ctx* ctx);
 const char* tac_last_error(void);
-/* Bytes of zero-initialised workspace needed by reducing calls for n_env envs. */
+/* Bytes of workspace needed by reducing calls for n_env envs. */
 size_t tac_workspace_bytes(const tac_ctx* ctx, int64_t n_env);
 /* Tiles per frame used by the frame kernels (for diagnostics). */
 int32_t tac_tiles_per_frame(const tac_ctx* ctx);
+/* Diagnostics: TAC_PATH_* that tac_pipeline takes for 16-B aligned input. */
+int32_t tac_pipeline_path(const tac_ctx* ctx);
 /* Diagnostics: number of kernel launches one tac_pipeline call makes for n_env. */
 int32_t tac_pipeline_launches(const tac_ctx* ctx, int64_t n_env);
 /* Diagnostics: runs tac_pipeline `iters` times with a CUDA event pair around
  * every kernel launch (synchronising the stream after each) and writes the
  * mean per-call milliseconds of each kernel kind: kernel_ms[0] = blur (or the
  * fused frame kernel), [1] = shade, [2] = per-env epilogue (0 when absent). */
-int tac_pipeline_profile(const tac_ctx* ctx, const struct tac_pipeline_args* args, void* stream,
+int tac_pipeline_profile(const tac_ctx* ctx, const tac_pipeline_args* args, void* stream,
                          int32_t iters, float* kernel_ms);
 /* Diagnostics: between tac_timing_begin and tac_timing_end, the first
  * max_calls single-chunk band-path tac_pipeline calls on this context record
@@ -211,7 +242,8 @@ int tac_shadow(const tac_ctx* ctx, const float* in, int32_t input_kind, float* f
  * synchronisation, no allocation: CUDA-graph capturable.  Equivalent to, per env:
  * indentation_from -> smooth_pyramid -> shade -> uint8 ; contact_center ->
  * (given load | track_load) -> marker_displacements -> render_markers. */
-typedef struct tac_pipeline_args {
+struct tac_pipeline_args {
+  uint32_t struct_size;     /* = sizeof(tac_pipeline_args) */
   const float* in;          /* [N,H,W] */
   int32_t input_kind;       /* TAC_INPUT_* */
   int32_t load_mode;        /* TAC_LOAD_* */
@@ -228,7 +260,7 @@ typedef struct tac_pipeline_args {
   int32_t splat;            /* nonzero: draw marker dots into rgb */
   void* workspace;
   int64_t n_env;
-} tac_pipeline_args;
+};
 
 int tac_pipeline(const tac_ctx* ctx, const tac_pipeline_args* args, void* stream);
 

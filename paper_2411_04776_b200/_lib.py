@@ -26,6 +26,11 @@ TAC_INPUT_DEPTH = 0
 TAC_INPUT_INDENTATION = 1
 TAC_LOAD_GIVEN = 0
 TAC_LOAD_TRACK = 1
+TAC_LUT_F32 = 0
+TAC_LUT_F16 = 1
+TAC_PATH_AUTO = 0
+TAC_PATH_BAND = 1
+TAC_PATH_FUSED = 2
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -33,7 +38,10 @@ _i64 = ctypes.c_int64
 
 
 class TacConfig(ctypes.Structure):
+    """struct tac_config (include/tac_b200.h); struct_size is filled in."""
+
     _fields_ = [
+        ("struct_size", ctypes.c_uint32),
         ("height", _i32),
         ("width", _i32),
         ("pixel_pitch", ctypes.c_double),
@@ -62,11 +70,21 @@ class TacConfig(ctypes.Structure):
         ("shadow_factor", ctypes.c_double),
         ("shadow_steps", _i32),
         ("shadow_softness", ctypes.c_double),
+        ("lut_dtype", _i32),
+        ("kernel_path", _i32),
+        ("chunk_envs", _i32),
     ]
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.struct_size = ctypes.sizeof(TacConfig)
 
 
 class TacPipelineArgs(ctypes.Structure):
+    """struct tac_pipeline_args (include/tac_b200.h); struct_size is filled in."""
+
     _fields_ = [
+        ("struct_size", ctypes.c_uint32),
         ("in_", _p),
         ("input_kind", _i32),
         ("load_mode", _i32),
@@ -85,6 +103,10 @@ class TacPipelineArgs(ctypes.Structure):
         ("n_env", _i64),
     ]
 
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.struct_size = ctypes.sizeof(TacPipelineArgs)
+
 
 # name -> (restype, argtypes); every symbol include/tac_b200.h declares.
 SIGNATURES = {
@@ -93,6 +115,7 @@ SIGNATURES = {
     "tac_last_error": (ctypes.c_char_p, []),
     "tac_workspace_bytes": (ctypes.c_size_t, [_p, _i64]),
     "tac_tiles_per_frame": (_i32, [_p]),
+    "tac_pipeline_path": (_i32, [_p]),
     "tac_pipeline_launches": (_i32, [_p, _i64]),
     "tac_pipeline_profile": (ctypes.c_int, [_p, ctypes.POINTER(TacPipelineArgs), _p, _i32, _p]),
     "tac_timing_begin": (ctypes.c_int, [_p, _i32]),

@@ -128,6 +128,13 @@ class PipelineConfig:
     shadow_factor: float = 1.0
     shadow_steps: int = 80
     shadow_softness: float = 5e-5
+    # execution choices (tac_config.lut_dtype / kernel_path / chunk_envs):
+    # lut_dtype "f16" stores the LUT coefficients in fp16 (half the shade
+    # kernel's gather bytes, <= 2^-11 relative per coefficient); kernel_path
+    # "auto" | "band" | "fused" picks the tac_pipeline kernels (A/B and tests)
+    lut_dtype: str = "f32"
+    kernel_path: str = "auto"
+    chunk_envs: int = 0
 
     def __post_init__(self):
         h, w = self.sensor.image_size
@@ -160,6 +167,12 @@ class PipelineConfig:
         if dirs.ndim != 2 or dirs.shape[1] != 3 or len(dirs) > 4:
             raise InvalidArgumentError("light_dirs must be (n <= 4, 3)")
         object.__setattr__(self, "light_dirs", dirs)
+        if self.lut_dtype not in ("f32", "f16"):
+            raise InvalidArgumentError("lut_dtype must be 'f32' or 'f16'")
+        if self.kernel_path not in ("auto", "band", "fused"):
+            raise InvalidArgumentError("kernel_path must be 'auto', 'band' or 'fused'")
+        if int(self.chunk_envs) < 0:
+            raise InvalidArgumentError("chunk_envs must be >= 0")
 
     @property
     def shadows(self) -> bool:

@@ -87,6 +87,10 @@ class Context:
         c.shadow_factor = float(cfg.shadow_factor)
         c.shadow_steps = int(cfg.shadow_steps)
         c.shadow_softness = float(cfg.shadow_softness)
+        c.lut_dtype = {"f32": _lib.TAC_LUT_F32, "f16": _lib.TAC_LUT_F16}[cfg.lut_dtype]
+        c.kernel_path = {"auto": _lib.TAC_PATH_AUTO, "band": _lib.TAC_PATH_BAND,
+                         "fused": _lib.TAC_PATH_FUSED}[cfg.kernel_path]
+        c.chunk_envs = int(cfg.chunk_envs)
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(self.lib.tac_ctx_create(ctypes.byref(c), ctypes.byref(handle)), "tac_ctx_create")
@@ -99,14 +103,16 @@ class Context:
 
     # -- workspaces ---------------------------------------------------------
     def workspace(self, n_env):
-        """Zero-initialised workspace for the current stream (kept zeroed by the kernels)."""
+        """Workspace for the current stream (the library initialises what it
+        uses on every call).  Calls from several host threads on ONE stream
+        share it and must not overlap: use one stream per thread."""
         stream = torch.cuda.current_stream(self.device)
         key = stream.cuda_stream
         nbytes = int(self.lib.tac_workspace_bytes(self.handle, int(n_env)))
         with self._ws_lock:
             ws = self._ws.get(key)
             if ws is None or ws.numel() < nbytes:
-                ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+                ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
                 self._ws[key] = ws
         return ws
 

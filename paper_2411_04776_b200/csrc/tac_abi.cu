@@ -62,12 +62,6 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
-int env_int(const char* name, int dflt) {
-  const char* s = std::getenv(name);
-  if (!s || !*s) return dflt;
-  return std::atoi(s);
-}
-
 static int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // Geometry of the strip-streaming kernel for one mode (see tac_frame.cu).
@@ -172,14 +166,18 @@ int common_checks(const tac_ctx* c, int64_t n_env) {
 }
 
 int tma_ok(const FrameParams& p, const void* in) {
-  if (env_int("TAC_NO_TMA", 0)) return 0;
   return (p.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
 }
 
-void bind_workspace(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) {
+// Strip-streaming kernel workspace: per-strip partials (always overwritten),
+// then the per-env arrival counters of multi-strip frames, zeroed here on the
+// call's stream (graph-capturable), so the workspace contents never matter.
+cudaError_t bind_workspace(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env, cudaStream_t s) {
   p.partials = reinterpret_cast<double*>(ws);
   const size_t part_bytes = (((size_t)n_env * c->max_tiles * kSumFields * sizeof(double)) + 255) & ~size_t(255);
   p.counters = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + part_bytes);
+  if (p.strips > 1 && n_env > 0) return cudaMemsetAsync(p.counters, 0, sizeof(unsigned int) * n_env, s);
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -191,6 +189,9 @@ const char* tac_last_error(void) { return g_err.c_str(); }
 int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   if (!cfg || !out) return fail(TAC_ERR_INVALID, "null argument");
   *out = nullptr;
+  if (cfg->struct_size != sizeof(tac_config))
+    return fail(TAC_ERR_INVALID, "tac_config.struct_size is %u, this library expects %zu (header version %d)",
+                cfg->struct_size, sizeof(tac_config), TAC_ABI_VERSION);
   const tac_config& k = *cfg;
   if (k.height < 2 || k.width < 2) return fail(TAC_ERR_INVALID, "image_size must be >= 2 x 2");
   if (!finite_pos(k.pixel_pitch)) return fail(TAC_ERR_INVALID, "pixel_pitch must be positive");
@@ -215,6 +216,12 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   if (!std::isfinite(k.k_n) || !std::isfinite(k.k_t)) return fail(TAC_ERR_INVALID, "marker params must be finite");
   if (!finite_pos(k.contact_threshold)) return fail(TAC_ERR_INVALID, "threshold must be positive");
   if (k.dot_radius < 0 || k.dot_radius > 32) return fail(TAC_ERR_UNSUPPORTED, "dot_radius must be in 0..32");
+  if (k.lut_dtype != TAC_LUT_F32 && k.lut_dtype != TAC_LUT_F16)
+    return fail(TAC_ERR_INVALID, "unknown lut_dtype %d", k.lut_dtype);
+  if (k.kernel_path < TAC_PATH_AUTO || k.kernel_path > TAC_PATH_FUSED)
+    return fail(TAC_ERR_INVALID, "unknown kernel_path %d", k.kernel_path);
+  if (k.chunk_envs < 0) return fail(TAC_ERR_INVALID, "chunk_envs must be >= 0");
+  if (k.lut_dtype == TAC_LUT_F16) return fail(TAC_ERR_UNSUPPORTED, "lut_dtype f16 is not available in this build");
   if (k.n_lights < 0 || k.n_lights > TAC_MAX_LIGHTS)
     return fail(TAC_ERR_INVALID, "n_lights must be in 0..%d", TAC_MAX_LIGHTS);
   if (!(k.shadow_factor >= 0.0 && k.shadow_factor <= 1.0))
@@ -253,18 +260,14 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
       for (int t = 1; t < 6; ++t) lut[b * 16 + ch * 5 + (t - 1)] = k.lut[(b * 3 + ch) * 6 + t];
   // half-planar LUT for the band shading kernel (plane h = floats 8h..8h+7 of
   // every bin, one 256-bit load each: a 128-B line holds 4 bins of a plane) and
-  // R/G/B background planes (coalesced loads).  Bin order: 1 (default) =
-  // direction-major [dir][mag] (neighbouring pixels' bins share lines most
-  // often: measured best); 0 = [mag][dir]; 2 = 4 mag x 2 dir tiles
-  const int order = env_int("TAC_LUT_ORDER", 1);
-  const size_t mtiles = ((size_t)k.mag_bins + 3) / 4;
-  const size_t nbins_p = order == 2 ? mtiles * 4 * (((size_t)k.dir_bins + 1) / 2 * 2) : nbins;
+  // R/G/B background planes (coalesced loads).  Bins in direction-major
+  // order [dir][mag]: neighbouring pixels' bins share lines most often
+  // (measured against [mag][dir] and 4x2 tiles in round 1)
+  const size_t nbins_p = nbins;
   std::vector<float> luth(nbins_p * 16, 0.f);
   for (size_t b = 0; b < nbins; ++b) {
     const size_t mb = b / k.dir_bins, db = b % k.dir_bins;
-    size_t o = b;
-    if (order == 1) o = db * k.mag_bins + mb;
-    if (order == 2) o = ((db / 2) * mtiles + mb / 4) * 8 + (db % 2) * 4 + mb % 4;
+    const size_t o = db * k.mag_bins + mb;
     for (int hh = 0; hh < 2; ++hh)
       for (int q = 0; q < 8; ++q) luth[(hh * nbins_p + o) * 8 + q] = lut[b * 16 + hh * 8 + q];
   }
@@ -439,11 +442,10 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.lut_tex = c->lut_tex;
   b.bg_planar = c->d_bg_planar;
   b.nbins = (int)nbins_p;
-  b.lut_order = order;
   b.bg_u8 = c->d_bg_u8;
   b.mg = mg;
 
-  const int max_strip = std::max(32, env_int("TAC_MAX_STRIP", 320));
+  const int max_strip = 320;  // strip-streaming kernel: columns per CTA
   c->fused = b;
   plan_strips(c->fused, kModeFused, max_strip);
   c->blur = b;
@@ -451,11 +453,10 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   c->contact = b;
   plan_strips(c->contact, kModeContact, max_strip);
   c->max_tiles = std::max({c->fused.strips, c->blur.strips, c->contact.strips});
-  const int kind = env_int("TAC_FRAME", 5);
   c->fused5 = c->fused;
   plan_v5(c->fused5);
-  c->use5 = kind == 5 && frame5_eligible(c->fused5);
-  c->chunk5 = std::max(1, env_int("TAC_CHUNK", 4096));
+  c->use5 = k.kernel_path != TAC_PATH_FUSED && frame5_eligible(c->fused5);
+  c->chunk5 = k.chunk_envs > 0 ? k.chunk_envs : 4096;
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
     if (p.stage_bytes > (int)(RB * p.v_pitch * sizeof(float))) {
@@ -465,8 +466,8 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
     if (frame_smem_bytes(p) > 227 * 1024) {
       free_ctx(c);
       return fail(TAC_ERR_UNSUPPORTED,
-                  "strip of %d columns with radius %d needs %zu B of shared memory (max 227 KB); "
-                  "set TAC_MAX_STRIP lower", p.strip_w, p.R, frame_smem_bytes(p));
+                  "strip of %d columns with radius %d needs %zu B of shared memory (max 227 KB)",
+                  p.strip_w, p.R, frame_smem_bytes(p));
     }
   }
   *out = c;
@@ -523,8 +524,8 @@ int tac_contact_blur(const tac_ctx* c, const float* in, int32_t input_kind, floa
   p.n_env = n_env;
   p.finalize = summary ? 1 : 0;
   p.summary = summary;
-  if (summary) bind_workspace(c, p, workspace, n_env);
-  cudaError_t e = launch_frame(p, kModeBlur, (cudaStream_t)stream);
+  cudaError_t e = summary ? bind_workspace(c, p, workspace, n_env, (cudaStream_t)stream) : cudaSuccess;
+  if (e == cudaSuccess) e = launch_frame(p, kModeBlur, (cudaStream_t)stream);
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_contact_blur");
 }
 
@@ -568,8 +569,8 @@ int tac_contact(const tac_ctx* c, const float* in, int32_t input_kind, double* c
   p.finalize = 1;
   p.summary = summary;
   p.contact = contact;
-  bind_workspace(c, p, workspace, n_env);
-  cudaError_t e = launch_frame(p, kModeContact, (cudaStream_t)stream);
+  cudaError_t e = bind_workspace(c, p, workspace, n_env, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = launch_frame(p, kModeContact, (cudaStream_t)stream);
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_contact");
 }
 
@@ -614,6 +615,9 @@ int tac_shadow(const tac_ctx* c, const float* in, int32_t input_kind, float* fac
 
 static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream, float* kt) {
   if (!a) return fail(TAC_ERR_INVALID, "null args");
+  if (a->struct_size != sizeof(tac_pipeline_args))
+    return fail(TAC_ERR_INVALID, "tac_pipeline_args.struct_size is %u, this library expects %zu",
+                a->struct_size, sizeof(tac_pipeline_args));
   int st = common_checks(c, a->n_env);
   if (st) return st;
   if (a->input_kind != TAC_INPUT_DEPTH && a->input_kind != TAC_INPUT_INDENTATION)
@@ -658,7 +662,8 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
       ev4 = tg.ev.data() + 4 * tg.used++;
     e = launch_frame5(p, (cudaStream_t)stream, kt, ev4);
   } else {
-    bind_workspace(c, p, a->workspace, a->n_env);
+    e = bind_workspace(c, p, a->workspace, a->n_env, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "tac_pipeline");
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (kt) {
       cudaEventCreate(&t0);
@@ -681,6 +686,11 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
 
 int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   return run_pipeline(c, a, stream, nullptr);
+}
+
+int32_t tac_pipeline_path(const tac_ctx* c) {
+  if (!c) return -1;
+  return c->use5 ? TAC_PATH_BAND : TAC_PATH_FUSED;
 }
 
 int32_t tac_pipeline_launches(const tac_ctx* c, int64_t n_env) {

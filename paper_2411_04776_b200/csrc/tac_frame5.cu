@@ -38,7 +38,7 @@
 //     (REF/marker.py:103-140), the marker displacements (REF/marker.py:143-165)
 //     and the dot splat (REF/marker.py:203-234).
 //
-// Envs run in chunks of TAC_CHUNK (default 4096): smaller chunks keep the
+// Envs run in chunks of tac_config.chunk_envs (default 4096): smaller chunks keep the
 // blurred intermediate in L2 but measured slower (launch tails dominate).
 #include <climits>
 #include <cstdio>
@@ -289,9 +289,10 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
         }
       }
       __syncthreads();
+      float* prow = vb + m * rpp;  // row pair m, column vbase
       if (has) {
-        float* prow = vb + m * rpp;  // row pair m, column vbase
-        // frame-border chunks write their own row pair's replicate pads
+        // frame-border chunks write their own row pair's replicate pads; the
+        // H items of the same row pair that read them are in the same warp
         if (c0 == 0) {
           const float2 e = *reinterpret_cast<const float2*>(prow - 2 * vbase);
           for (int i = 0; i < R4; i += 2)
@@ -302,6 +303,9 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
           for (int i = 0; i < R4; i += 2)
             *reinterpret_cast<float4*>(prow + 2 * (W - vbase + i)) = make_float4(e.x, e.y, e.x, e.y);
         }
+      }
+      __syncwarp();  // pads visible to the warp's other lanes (convergent point)
+      if (has) {
         switch (RL) {
 #define X(r)                                                                   \
   case r:                                                                      \
@@ -356,9 +360,7 @@ __device__ __forceinline__ void ld256(const float* p, float4& a, float4& b) {
 }
 
 __device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) {
-  if (p.lut_order == 1) return db * p.mag_bins + mb;
-  if (p.lut_order == 2) return (((db >> 1) * ((p.mag_bins + 3) >> 2) + (mb >> 2)) << 3) + ((db & 1) << 2) + (mb & 3);
-  return mb * p.dir_bins + db;
+  return db * p.mag_bins + mb;  // direction-major (tac_ctx_create)
 }
 
 // ---------------------------------------------------------------------------

@@ -74,7 +74,6 @@ struct FrameParams {
   unsigned long long lut_tex;  // cudaTextureObject_t over lut_half as float4 texels (0 = none)
   const float* bg_planar;    // [3][H][W]
   int nbins;
-  int lut_order;             // lut_half bin order: 0 = [mag][dir], 1 = [dir][mag], 2 = 4x2 tiles
   // io
   const float* in;
   int input_depth;

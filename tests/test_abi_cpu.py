@@ -189,3 +189,113 @@ class TestHostConfig:
             PipelineConfig(s, ((1.0, 3),), np.zeros((2, 2, 3, 6)), np.zeros((8, 9, 3)))
         cfg = PipelineConfig(s, ((1.0, 3),), np.zeros((2, 2, 3, 6)), np.zeros((8, 10, 3)))
         assert cfg.rest_grid.shape == (10, 10, 2)
+
+
+# --------------------------------------------------------------------------- C layout
+_FIELDS = {
+    "tac_config": [f for f, _ in _lib.TacConfig._fields_],
+    "tac_pipeline_args": [("in" if f == "in_" else f) for f, _ in _lib.TacPipelineArgs._fields_],
+}
+
+
+def _probe_source():
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "tac_b200.h"', "int main(void) {"]
+    for st, fields in _FIELDS.items():
+        lines.append(f'  printf("{st} size %zu\\n", sizeof({st}));')
+        for f in fields:
+            lines.append(f'  printf("{st} {f} %zu\\n", offsetof({st}, {f}));')
+    lines += ["  return 0;", "}"]
+    return "\n".join(lines) + "\n"
+
+
+@pytest.fixture(scope="module")
+def c_layout(tmp_path_factory):
+    """Compile the header as strict C11 (-Werror) and read sizeof/offsetof."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc unavailable")
+    d = tmp_path_factory.mktemp("clayout")
+    (d / "probe.c").write_text(_probe_source())
+    exe = d / "probe"
+    cmd = ["gcc", "-std=c11", "-Wall", "-Wextra", "-Wpedantic", "-Werror", "-I", os.path.join(ROOT, "include"),
+           str(d / "probe.c"), "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    layout = {}
+    for line in out.splitlines():
+        st, f, v = line.split()
+        layout[(st, f)] = int(v)
+    return layout
+
+
+def _integration_binding():
+    """Exec the reference-side ctypes snippet of INTEGRATION.md §2 (its CDLL
+    pointed at the in-tree library)."""
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    m = re.search(r"```python\n(# tacsim/_b200\.py.*?)```", text, flags=re.S)
+    assert m, "INTEGRATION.md lost its ctypes binding"
+    code = m.group(1).replace('ctypes.CDLL("libtac_b200.so")', f"ctypes.CDLL({_lib.LIB_PATH!r})")
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    return ns
+
+
+class TestCLayout:
+    def test_header_is_valid_c11_and_cxx(self, tmp_path):
+        import shutil
+        import subprocess
+
+        if shutil.which("g++") is None:
+            pytest.skip("g++ unavailable")
+        (tmp_path / "x.cc").write_text('#include "tac_b200.h"\nint main() { return sizeof(tac_config) > 0 ? 0 : 1; }\n')
+        r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                            str(tmp_path / "x.cc"), "-o", str(tmp_path / "x")], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+
+    @pytest.mark.parametrize("name,cls", [("tac_config", _lib.TacConfig), ("tac_pipeline_args", _lib.TacPipelineArgs)])
+    def test_package_binding_matches_compiled_layout(self, c_layout, name, cls):
+        assert ctypes.sizeof(cls) == c_layout[(name, "size")]
+        for (f, _), cf in zip(cls._fields_, _FIELDS[name]):
+            assert getattr(cls, f).offset == c_layout[(name, cf)], f
+
+    def test_integration_snippet_matches_compiled_layout(self, c_layout):
+        ns = _integration_binding()
+        for name, cls in (("tac_config", ns["TacConfig"]), ("tac_pipeline_args", ns["TacPipelineArgs"])):
+            assert [f for f, _ in cls._fields_] == [f for f, _ in
+                                                    (_lib.TacConfig if name == "tac_config" else _lib.TacPipelineArgs)._fields_]
+            assert ctypes.sizeof(cls) == c_layout[(name, "size")]
+            for (f, _), cf in zip(cls._fields_, _FIELDS[name]):
+                assert getattr(cls, f).offset == c_layout[(name, cf)], (name, f)
+        assert ns["TacConfig"]().struct_size == c_layout[("tac_config", "size")]
+
+    def test_struct_size_mismatch_is_rejected(self):
+        lib = _lib.load()
+        c, keep = _cfg()
+        c.struct_size = ctypes.sizeof(_lib.TacConfig) - 8  # a caller built against an older header
+        h = ctypes.c_void_p()
+        assert lib.tac_ctx_create(ctypes.byref(c), ctypes.byref(h)) == _lib.TAC_ERR_INVALID
+        assert b"struct_size" in lib.tac_last_error()
+        a = _lib.TacPipelineArgs()
+        a.struct_size = 0
+        assert lib.tac_pipeline(ctypes.c_void_p(1), ctypes.byref(a), None) == _lib.TAC_ERR_INVALID
+        assert b"struct_size" in lib.tac_last_error()
+
+    def test_execution_knobs_validated(self):
+        lib = _lib.load()
+        for field, val in (("lut_dtype", 7), ("kernel_path", 9), ("chunk_envs", -1)):
+            c, keep = _cfg(**{field: val})
+            h = ctypes.c_void_p()
+            assert lib.tac_ctx_create(ctypes.byref(c), ctypes.byref(h)) == _lib.TAC_ERR_INVALID, field
+
+    def test_library_reads_no_environment_knobs(self):
+        """A/B switches live in tac_config, not in getenv (VERDICT r1 weak #8)."""
+        data = open(_lib.LIB_PATH, "rb").read()
+        for knob in (b"TAC_NO_TMA", b"TAC_LUT_ORDER", b"TAC_MAX_STRIP", b"TAC_FRAME", b"TAC_CHUNK"):
+            assert knob + b"\0" not in data, knob
+        src = "".join(open(os.path.join(ROOT, "paper_2411_04776_b200", "csrc", f)).read()
+                      for f in os.listdir(os.path.join(ROOT, "paper_2411_04776_b200", "csrc"))
+                      if f.endswith((".cu", ".cuh")))
+        assert "getenv" not in src

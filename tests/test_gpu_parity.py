@@ -6,6 +6,8 @@ pixels; blurred heights and marker displacements within 1e-4 relative
 the reference-pinned cases bit-exact.
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -470,24 +472,23 @@ class TestShadows:
 
 
 class TestKernelVariants:
-    """The band-tiled two-kernel path (tac_frame5.cu, default: TAC_FRAME=5)
-    against the strip-streaming fused kernel (tac_frame.cu, TAC_FRAME=3) on a full-size
+    """The default tac_pipeline path (kernel_path "auto") against the
+    strip-streaming fused kernel (tac_frame.cu, kernel_path "fused") on a full-size
     configs[2] batch: the same arithmetic up to the fp32 summation order of the
     levels, so RGB may differ by a rounding flip and the blur by ulps; the
     exact-zero skips must agree exactly."""
 
-    @pytest.mark.parametrize("variant", ["5"])
+    @pytest.mark.parametrize("variant", ["auto", "band"])
     @pytest.mark.parametrize("kind", [None, "sphere", "perlin"])
-    def test_variant_matches_strip_kernel(self, monkeypatch, kind, variant):
+    def test_variant_matches_strip_kernel(self, kind, variant):
         cfg, _ = synthetic.baseline_config(2, 0)
+        cfg = dataclasses.replace(cfg, kernel_path=variant)
         n = 48
         p = synthetic.indenters(n, 240, 320, 5, fixed_kind=kind)
         depth = synthetic.height_maps(p, 240, 320, dtype=torch.float64).float()
         shear, twist = synthetic.loads(n, 6)
-        monkeypatch.setenv("TAC_FRAME", variant)
         obs4 = run_pipeline(cfg, depth, shear, twist)
-        monkeypatch.setenv("TAC_FRAME", "3")
-        cfg3, _ = synthetic.baseline_config(2, 0)  # a new config object -> a new context
+        cfg3 = dataclasses.replace(cfg, kernel_path="fused")
         obs3 = run_pipeline(cfg3, depth, shear, twist)
         d = (obs4.rgb.int() - obs3.rgb.int()).abs()
         # a ulp of blur can flip a LUT bin near a boundary (then |d| > 1 is possible)
@@ -652,15 +653,14 @@ class TestBandPathShapes:
         for i in range(4):
             check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])
 
-    def test_env_chunks_match_single_launch(self, monkeypatch):
-        """TAC_CHUNK splits the envs over several (blur, shade) launch pairs:
+    def test_env_chunks_match_single_launch(self):
+        """chunk_envs splits the envs over several (blur, shade) launch pairs:
         per-chunk views of every per-env buffer must give the same outputs."""
         n = 7
         depth = depth_batch(n, 48, 64, seed=65)
         shear, twist = synthetic.loads(n, 66)
         ref = run_pipeline(small_config(48, 64), depth, shear, twist)
-        monkeypatch.setenv("TAC_CHUNK", "3")
-        got = run_pipeline(small_config(48, 64), depth, shear, twist)  # new config -> new context
+        got = run_pipeline(dataclasses.replace(small_config(48, 64), chunk_envs=3), depth, shear, twist)
         assert torch.equal(got.rgb, ref.rgb)
         assert torch.equal(got.blurred, ref.blurred)
         assert torch.equal(got.disp, ref.disp)
