@@ -1,16 +1,18 @@
 #!/usr/bin/env python
 """Throughput bench of the B200 tactile path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (bench.py --gpus N > 1 launches this itself)
 
-Workload (N=1): BASELINE configs[2] -- 4096 envs of 240x320 synthetic height
-maps (sphere / cylinder / cube edge / Perlin plate, penetration U(0, 1.2 mm)),
-sigma (1,2,4) pyramid, 125x180 random LUT, U[80,160] background, 7x9
-markers with random shear/twist, dots r=3.  One step = one ``tac_pipeline``
-call over all envs (band blur, band shade, per-env epilogue launches).  N>1:
-every rank runs its own 4096-env block (weak scaling; at N=8 that is configs[4]'s 32768 envs) plus the NCCL
-all-gather of the [N, 8] contact summaries once per step.
+Workload (default): BASELINE configs[4] -- 32768 envs of 240x320 synthetic
+height maps (sphere / cylinder / cube edge / Perlin plate, penetration
+U(0, 1.2 mm)), sigma (1,2,4) pyramid, 125x180 random LUT, U[80,160]
+background, 7x9 markers with random shear/twist, dots r=3, split evenly over
+the N GPUs by ``sharding.env_block`` (strong scaling: N=1 runs all 32768 envs
+on one GPU).  One step = one ``tac_pipeline`` call over the rank's env block
+and, for N>1, the NCCL all-gather of the [32768, 8] contact summaries (on a
+side stream, inside the timed region).  ``--config 1|2|3`` runs the other
+BASELINE configs the same way (their global env counts).
 
 Prints ONE JSON line (rank 0).
 """
@@ -38,25 +40,55 @@ UNIT = "frames/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[i] (1, 2 or 3)")
-    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0, help="cpu_baseline sample (wall s)")
+    ap.add_argument("--config", type=int, default=4, help="BASELINE.json configs[i] (1..4)")
+    ap.add_argument("--envs", type=int, default=0, help="override the global env count")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample (wall s)")
     ap.add_argument("--ref-seconds", type=float, default=90.0, help="--impl reference total budget (wall s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shadows", action="store_true", help="add_shadows on (REF/optical.py:261-300)")
+    ap.add_argument("--lut-dtype", default="f32", choices=["f32", "f16"])
+    ap.add_argument("--kernel-path", default="auto", choices=["auto", "band", "fused"])
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
+
+
+def bench_config(a):
+    """(PipelineConfig, n_total, params, shear, twist) of the run's workload."""
+    import dataclasses
+
+    from paper_2411_04776_b200 import synthetic
+
+    cfg, n, params, shear, twist = synthetic.workload(a.config, a.seed, a.envs or None)
+    over = dict(lut_dtype=a.lut_dtype, kernel_path=a.kernel_path)
+    if a.shadows:
+        over.update(light_dirs=default_light_dirs(), shadow_factor=0.6)
+    return dataclasses.replace(cfg, **over), n, params, shear, twist
+
+
+def default_light_dirs():
+    """tacsim default_lighting() directions (REF/optical.py:68-79): three lights
+    120 degrees apart in azimuth at 35 degrees elevation, unit length."""
+    el = math.radians(35.0)
+    d = np.array([[math.cos(el) * math.cos(t), math.cos(el) * math.sin(t), math.sin(el)]
+                  for t in np.deg2rad([0.0, 120.0, 240.0])])
+    return d / np.linalg.norm(d, axis=-1, keepdims=True)
+
+
+def workload_name(a):
+    return f"configs[{a.config}]" + (" + shadows" if a.shadows else "")
 
 
 # --------------------------------------------------------------------------- CPU arm
 _W = {}
 
 
-def _cpu_init(cfg_index, seed, worker_frames):
-    """Pool initializer: one single-threaded process holding a few distinct frames."""
+def _cpu_init(a, env_ids):
+    """Pool initializer: one single-threaded process holding a few frames of
+    the GPU run's own workload (env indices ``env_ids``, same seeds)."""
     os.environ["OMP_NUM_THREADS"] = "1"
     import torch
 
@@ -64,12 +96,14 @@ def _cpu_init(cfg_index, seed, worker_frames):
     from oracle.fast import FastOracle
     from paper_2411_04776_b200 import synthetic
 
-    cfg, _ = synthetic.baseline_config(cfg_index, seed)
+    cfg, n, params, shear, twist = bench_config(a)
     h, w = cfg.sensor.image_size
-    rank = os.getpid() % 1000
-    p = synthetic.indenters(worker_frames, h, w, seed + 10 + rank)
-    _W["depth"] = synthetic.height_maps(p, h, w, dtype=torch.float64).numpy()
-    _W["shear"], _W["twist"] = synthetic.loads(worker_frames, seed + 20 + rank)
+    # each worker takes its own share of the sample (by process start order)
+    ident = mproc.current_process()._identity
+    k = (ident[0] - 1) if ident else 0
+    mine = env_ids[k % len(env_ids)]
+    _W["depth"] = synthetic.height_maps(params.subset(mine), h, w, dtype=torch.float64).numpy()
+    _W["shear"], _W["twist"] = shear[mine], twist[mine]
     _W["orc"] = FastOracle(cfg)
     _W["orc"].run(_W["depth"][0], _W["shear"][0], _W["twist"][0])  # warm
 
@@ -86,12 +120,19 @@ def _cpu_job(count):
 
 class CpuArm:
     """A process pool (one single-threaded worker per host core) timing the
-    oracle port of the reference CPU path on configs[i] frames."""
+    oracle port of the reference CPU path on frames of the bench workload:
+    worker k holds envs sample[k::cores] (an evenly strided sample of all
+    envs, so every indenter kind and pose mix is represented)."""
 
-    def __init__(self, cfg_index, seed, cores, worker_frames=8):
+    def __init__(self, a, cores, worker_frames=8):
+        cfg, n, *_ = bench_config(a)
         self.cores = cores
+        k = min(n, cores * worker_frames)
+        sample = np.unique(np.linspace(0, n - 1, k).round().astype(np.int64))
+        self.env_ids = [sample[c::cores] for c in range(cores) if len(sample[c::cores])]
+        self.n_sample = len(sample)
         ctx = mproc.get_context("spawn")
-        self.pool = ctx.Pool(cores, initializer=_cpu_init, initargs=(cfg_index, seed, worker_frames))
+        self.pool = ctx.Pool(cores, initializer=_cpu_init, initargs=(a, self.env_ids))
         self.per_frame = max(r[1] / r[0] for r in self.pool.map(_cpu_job, [2] * cores))
 
     def step(self, frames_per_core):
@@ -101,6 +142,13 @@ class CpuArm:
         wall = time.perf_counter() - t0
         frames = sum(r[0] for r in res)
         return frames / wall, statistics.mean(r[0] / r[1] for r in res), wall, frames
+
+    def describe(self, a, fpc):
+        return (f"{self.cores}x{fpc} frames per step, cycling {self.n_sample} distinct envs (an even stride "
+                f"over the {workload_name(a)} workload, same seeds as the GPU run); oracle port "
+                "(scipy.ndimage.gaussian_filter as REF/tactile.py:219, numpy gradient/LUT/markers as "
+                "REF/optical.py:160-250, REF/marker.py:103-234" + (", add_shadows REF/optical.py:261-300" if a.shadows
+                                                                  else "") + "), f64")
 
     def close(self):
         self.pool.close()
@@ -180,12 +228,11 @@ def measured_peak():
 
 
 def fma_per_frame(cfg):
-    """Dense FFMA count per frame of the strip-streaming blur: per level a
-    vertical and a horizontal pass of (2r+1) taps over every pixel of the
-    16-row blocks (zero-block skips not counted)."""
+    """Dense FMA count per frame of the separable pyramid: per level a
+    vertical and a horizontal pass of (2r+1) taps over every pixel (zero
+    columns the kernels skip exactly are counted: "dense equivalent")."""
     h, w = cfg.sensor.image_size
-    rows = -(-h // 16) * 16
-    return sum(2 * (2 * r + 1) * rows * w for _, r in cfg.levels if r)
+    return sum(2 * (2 * r + 1) * h * w for _, r in cfg.levels if r)
 
 
 def algorithmic_bytes(cfg):
@@ -195,8 +242,9 @@ def algorithmic_bytes(cfg):
     return 4 * h * w + 3 * h * w + 8 * r * c + 32
 
 
-def kernel_bytes(cfg):
-    """Algorithmic HBM bytes per frame of each kernel of the two-kernel path
+def kernel_bytes(cfg, pipe):
+    """Algorithmic HBM bytes per frame of each kernel kind of the pipeline
+    call, in the order tac_timing_end reports them [blur, shade, epilogue]
     (DESIGN.md §5): blur = depth in + blurred out + band partials; shade =
     blurred in + RGB out (the LUT and background are shared, L2-resident);
     epilogue = partials in + marker field + summary out + dot pixels RMW."""
@@ -205,21 +253,56 @@ def kernel_bytes(cfg):
     bands = -(-h // 16)
     rr = cfg.dot_radius
     dot_px = sum(1 for dy in range(-rr, rr + 1) for dx in range(-rr, rr + 1) if dx * dx + dy * dy <= rr * rr)
+    names = pipe.kernel_names()
+    if len(names) == 1:  # one fused frame kernel
+        return {names[0]: algorithmic_bytes(cfg)}
+    return dict(zip(names, (4 * h * w + 4 * h * w + 64 * bands,
+                            4 * h * w + 3 * h * w,
+                            64 * bands + 8 * r * c + 32 + 3 * dot_px * r * c)))
+
+
+# --------------------------------------------------------------------------- arms
+def base_line(a, world, n_total):
+    """Keys shared by both arms' JSON lines."""
+    from paper_2411_04776_b200.sharding import env_block
+
+    cfg = bench_config(a)[0]
+    h, w = cfg.sensor.image_size
     return {
-        "band_blur_kernel": 4 * h * w + 4 * h * w + 64 * bands,
-        "band_shade_kernel": 4 * h * w + 3 * h * w,
-        "env_epilogue_kernel": 64 * bands + 8 * r * c + 32 + 3 * dot_px * r * c,
+        "metric": METRIC,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "data": "synthetic (seeded indenter height maps; BASELINE names no dataset)",
+        "config": {
+            "workload": workload_name(a),
+            "global_envs": n_total,
+            "envs_per_gpu": env_block(0, world, n_total)[1],
+            "H": h, "W": w,
+            "sigmas": [s for s, _ in cfg.levels],
+            "lut_bins": list(cfg.lut.shape[:2]),
+            "lut_dtype": cfg.lut_dtype,
+            "markers": list(cfg.sensor.marker_grid),
+            "dot_radius": cfg.dot_radius,
+            "shadows": bool(cfg.shadows),
+        },
     }
 
 
 # --------------------------------------------------------------------------- arms
 def run_reference(a, rank, world):
     """--impl reference: the oracle port of the reference CPU path on all host
-    cores, each step a bounded sample so the whole run stays within minutes."""
+    cores, each step a bounded sample of the same workload so the whole run
+    stays within minutes.  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
+    cfg, n_total, *_ = bench_config(a)
     cores = host_cores()
-    arm = CpuArm(a.config, a.seed, cores)
+    arm = CpuArm(a, cores)
     budget = max(0.5, a.ref_seconds / max(1, a.steps + a.warmup))  # wall seconds per step
     fpc = max(1, int(budget / arm.per_frame))
     for _ in range(a.warmup):
@@ -231,32 +314,13 @@ def run_reference(a, rank, world):
         walls.append(wall)
     arm.close()
     v = statistics.median(vals)
-    from paper_2411_04776_b200 import synthetic
-
-    cfg, n_env = synthetic.baseline_config(a.config, a.seed)
-    line = {
-        "impl": "reference",
-        "metric": METRIC,
-        "value": v,
-        "unit": UNIT,
-        "n_gpus": world,
-        "steps": a.steps,
-        "warmup": a.warmup,
-        "ms_per_step": 1e3 * statistics.median(walls),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"configs[{a.config}] sample", "frames_per_step": cores * fpc,
-                   "H": cfg.sensor.image_size[0], "W": cfg.sensor.image_size[1],
-                   "sigmas": [s for s, _ in cfg.levels], "markers": list(cfg.sensor.marker_grid),
-                   "parallelism": f"cpu x{cores} processes"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{cores}x{fpc} frames of configs[{a.config}] per step, oracle port "
-                                   "(scipy.ndimage blur as REF/tactile.py:219, numpy gradient/LUT/markers), f64"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    line = {"impl": "reference", **base_line(a, world, n_total)}
+    line.update(value=v, ms_per_step=1e3 * statistics.median(walls), dtype="f64")
+    line["config"]["parallelism"] = f"cpu x{cores} processes"
+    line["config"]["frames_per_step"] = cores * fpc
+    line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": arm.describe(a, fpc)}
+    line["e2e"] = {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
 
 
@@ -266,35 +330,42 @@ def run_ours(a, rank, world, local_rank):
 
     from paper_2411_04776_b200 import TactilePipeline, synthetic
     from paper_2411_04776_b200.hostio import HostStreamer, host_observation
-    from paper_2411_04776_b200.sharding import gather_summaries
+    from paper_2411_04776_b200.sharding import env_block, gather_summaries
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    cfg, n_env = synthetic.baseline_config(a.config, a.seed)
-    if a.envs:
-        n_env = a.envs
+    cfg, n_total, params, shear_np, twist_np = bench_config(a)
     h, w = cfg.sensor.image_size
+    e0, e1 = env_block(rank, world, n_total)
+    n_env = e1 - e0
+    blk = -(-n_total // world)  # all-gather block (ragged splits are padded)
     pipe = TactilePipeline(cfg, dev)
 
-    # inputs resident in HBM before the timed region (> L2, see config.l2)
-    params = synthetic.indenters(n_env, h, w, a.seed + 10 + 1000 * rank)
-    depth = synthetic.height_maps(params, h, w, device=dev, dtype=torch.float32, chunk=512)
-    shear_np, twist_np = synthetic.loads(n_env, a.seed + 20 + 1000 * rank)
-    shear = torch.as_tensor(shear_np, device=dev)
-    twist = torch.as_tensor(twist_np, device=dev)
+    # this rank's env block of the global workload, resident in HBM before the
+    # timed region (> L2, see config.l2)
+    depth = synthetic.height_maps(params.subset(slice(e0, e1)), h, w, device=dev, dtype=torch.float32, chunk=512)
+    shear = torch.as_tensor(shear_np[e0:e1], device=dev)
+    twist = torch.as_tensor(twist_np[e0:e1], device=dev)
     out = pipe.allocate(n_env)
     args = pipe.launch_args(depth, shear, twist, out)
-    gathered = torch.empty((world * n_env, 8), dtype=torch.float32, device=dev) if world > 1 else None
     if world > 1:
         # the once-per-step NCCL all-gather of the [N, 8] summaries runs on a side
         # stream, overlapping the next step's kernels; summaries are double-buffered
+        gathered = torch.empty((world * blk, 8), dtype=torch.float32, device=dev)
+        summ_ab = [torch.zeros((blk, 8), dtype=torch.float32, device=dev) for _ in range(2)]
         out2 = pipe.allocate(n_env)
-        args_ab = [args, pipe.launch_args(depth, shear, twist, out2)]
-        summ_ab = [out.summary, out2.summary]
+        out.summary, out2.summary = summ_ab[0][:n_env], summ_ab[1][:n_env]
+        args_ab = [pipe.launch_args(depth, shear, twist, out), pipe.launch_args(depth, shear, twist, out2)]
+        args = args_ab[0]
         side = torch.cuda.Stream(dev)
         done = [torch.cuda.Event(), torch.cuda.Event()]   # pipeline k finished (side waits)
         freed = [torch.cuda.Event(), torch.cuda.Event()]  # gather k finished (main waits before k+2)
         k_step = [0]
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)  # communicator up before anything is timed
+        if rank == 0:
+            print(f"nccl communicator: nranks={dist.get_world_size()} backend={dist.get_backend()}",
+                  file=sys.stderr, flush=True)
 
     def step():
         if world == 1:
@@ -342,78 +413,77 @@ def run_ours(a, rank, world, local_rank):
         ms = float(t.item())
         dist.barrier()
     ms_step = ms / a.steps
-    value = world * n_env * a.steps / (ms / 1e3)
+    value = n_total * a.steps / (ms / 1e3)
 
     # one tac_pipeline call (all its launches) bracketed by events on the launch stream
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
-    for e0, e1 in kev:
-        e0.record(stream)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    for k0, k1 in kev:
+        k0.record(stream)
         pipe.launch(args)
-        e1.record(stream)
+        k1.record(stream)
     torch.cuda.synchronize()
-    k_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in kev)
-    # per-kernel durations: the in-region boundary events; the fused path
-    # records none and falls back to events around each launch, synchronised
-    # per launch (tac_pipeline_profile)
+    k_ms = statistics.mean(k0.elapsed_time(k1) for k0, k1 in kev)
+    # per-kernel durations: the in-region boundary events (summed per call over
+    # its env chunks); the fused path falls back to tac_pipeline_profile
     if region_calls == a.steps:
         kern_ms, kern_src = region_ms, f"CUDA events at the kernel boundaries of the {a.steps} timed calls"
     else:
-        kern_ms, kern_src = pipe.profile(args, iters=10), "tac_pipeline_profile (10 calls, synchronised per launch)"
+        kern_ms, kern_src = pipe.profile(args, iters=5), "tac_pipeline_profile (5 calls, in-stream events)"
     launches = pipe.launches_per_call(n_env)
 
     # e2e: host buffers through the public host API, copies inside the timed region
     e2e = None
     if not a.no_e2e:
-        depth_h = depth.cpu().pin_memory()
-        shear_h = shear.cpu().pin_memory()
-        twist_h = twist.cpu().pin_memory()
+        pin = dict(pin_memory=True)
+        depth_h = torch.empty(tuple(depth.shape), dtype=depth.dtype, **pin)
+        depth_h.copy_(depth)
+        shear_h = torch.empty(tuple(shear.shape), dtype=shear.dtype, **pin)
+        shear_h.copy_(shear)
+        twist_h = torch.empty(tuple(twist.shape), dtype=twist.dtype, **pin)
+        twist_h.copy_(twist)
         out_h = host_observation(pipe, n_env)
         streamer = HostStreamer(pipe, chunk=min(256, n_env))  # tools/e2e_sweep.py: best measured
-        e_steps = max(3, min(20, a.steps // 10))
+        e_steps = max(3, min(10, a.steps // 10))
         for _ in range(2):
             streamer.run(depth_h, shear_h, twist_h, out_h)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
         for _ in range(e_steps):
             streamer.run(depth_h, shear_h, twist_h, out_h)
-        e1.record(stream)
+        x1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
+        ems = x0.elapsed_time(x1)
         if world > 1:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         r, c = cfg.sensor.marker_grid
         e2e = {
-            "value": world * n_env * e_steps / (ems / 1e3),
+            "value": n_total * e_steps / (ems / 1e3),
             "unit": UNIT,
-            "h2d_bytes_per_step": n_env * (4 * h * w + 16 + 8),
-            "d2h_bytes_per_step": n_env * (3 * h * w + 8 * r * c + 32),
+            "h2d_bytes_per_step": n_total * (4 * h * w + 16 + 8),
+            "d2h_bytes_per_step": n_total * (3 * h * w + 8 * r * c + 32),
             "steps": e_steps,
             "path": "hostio.HostStreamer -> TactilePipeline.simulate (tac_pipeline C ABI), pinned host buffers",
-            "h2d_gbs": n_env * (4 * h * w + 16 + 8) * e_steps / (ems / 1e3) / 1e9,
+            "h2d_gbs_per_gpu": n_env * (4 * h * w + 16 + 8) * e_steps / (ems / 1e3) / 1e9,
         }
+        del depth_h, out_h
 
     if rank != 0:
         return
     peak, peak_kind = measured_peak()
     per_launch = algorithmic_bytes(cfg) * n_env
     step_gbs = per_launch / (k_ms / 1e3) / 1e9
-    kb = kernel_bytes(cfg)
+    kb = kernel_bytes(cfg, pipe)
     kernels = {}
-    if launches > 1:  # two-kernel path (tac_frame5.cu)
-        for name, kms in zip(kb, kern_ms):
-            if kms > 0:
-                gbs = kb[name] * n_env / (kms / 1e3) / 1e9
-                kernels[name] = {"ms": kms, "bytes_per_frame": kb[name], "achieved_gbs": gbs, "frac": gbs / peak}
-        dom = max(kernels, key=lambda k: kernels[k]["ms"])
-    else:  # one fused kernel (TAC_FRAME=3)
-        dom = "frame_kernel (fused)"
-        kernels[dom] = {"ms": kern_ms[0], "bytes_per_frame": algorithmic_bytes(cfg),
-                        "achieved_gbs": step_gbs, "frac": step_gbs / peak}
+    for name, kms in zip(kb, kern_ms):
+        if kms > 0:
+            gbs = kb[name] * n_env / (kms / 1e3) / 1e9
+            kernels[name] = {"ms": kms, "bytes_per_frame": kb[name], "achieved_gbs": gbs, "frac": gbs / peak}
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
     achieved = kernels[dom]["achieved_gbs"]
     props = torch.cuda.get_device_properties(dev)
     clocks = clk.result()
@@ -424,87 +494,85 @@ def run_ours(a, rank, world, local_rank):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            t = json.load(open(tpath)).get(f"configs[{a.config}]")
+            t = json.load(open(tpath)).get(workload_name(a))
             traffic = t.get(dom) if isinstance(t, dict) else None
             if traffic is not None:
                 traffic = traffic * n_env / t.get("envs", n_env)  # scale to this launch size
         except Exception:
             traffic = None
-    line = {
-        "metric": METRIC,
-        "value": value,
-        "unit": UNIT,
-        "n_gpus": world,
-        "steps": a.steps,
-        "warmup": a.warmup,
-        "ms_per_step": ms_step,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic (seeded indenter height maps generated on device; no dataset exists)",
-        "config": {
-            "workload": f"configs[{a.config}]",
-            "envs_per_gpu": n_env,
-            "global_envs": world * n_env,
-            "H": h, "W": w,
-            "sigmas": [s for s, _ in cfg.levels],
-            "lut_bins": list(cfg.lut.shape[:2]),
-            "markers": list(cfg.sensor.marker_grid),
-            "dot_radius": cfg.dot_radius,
-            "parallelism": f"env-sharded x{world}" + (" + NCCL all_gather(summary) on a side stream" if world > 1 else ""),
-            "l2": f"inputs {n_env * h * w * 4 / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)",
-            "contact_pixel_fraction": round(contact_frac, 4),
-        },
-        "roofline": {
-            "bound": "hbm",
-            "achieved": achieved,
-            "peak": peak,
-            "unit": "GB/s",
-            "frac": achieved / peak,
-            "traffic": traffic,
-            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)",
-            "kernel": dom,
-            "kernel_timing": kern_src,
-            "kernel_ms": kernels[dom]["ms"],
-            "algorithmic_bytes_per_launch": kernels[dom]["bytes_per_frame"] * n_env,
-            "kernels": kernels,
-            "step": {"ms": k_ms, "algorithmic_bytes_per_frame": algorithmic_bytes(cfg),
-                     "achieved_gbs": step_gbs, "frac": step_gbs / peak},
-            # pyramid FMAs of a dense frame (zero columns are skipped, so "dense
-            # equivalent"): over the whole step and over the blur kernel alone
-            "fp32_fma": {"per_frame_dense": fma,
-                         "achieved_tflops_dense_equiv": 2 * fma * n_env / (k_ms / 1e3) / 1e12,
-                         "blur_kernel_tflops_dense_equiv": 2 * fma * n_env / (kernels[BLUR]["ms"] / 1e3) / 1e12
-                         if BLUR in kernels else None,
-                         "peak_tflops": 2 * fma_peak / 1e12},
-        },
-        "gpu_launches": a.steps * launches,
-        "clocks": clocks,
-        "device": props.name,
+    line = base_line(a, world, n_total)
+    line.update(value=value, ms_per_step=ms_step, dtype="f32")
+    line["config"].update({
+        "kernel_path": pipe.path_name(),
+        "parallelism": f"env-sharded x{world} (sharding.env_block)" +
+                       (" + NCCL all_gather(summary) on a side stream" if world > 1 else ""),
+        "l2": f"inputs {n_env * h * w * 4 / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)",
+        "contact_pixel_fraction": round(contact_frac, 4),
+    })
+    line["roofline"] = {
+        "bound": "hbm",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": achieved / peak,
+        "traffic": traffic,
+        "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)",
+        "kernel": dom,
+        "kernel_timing": kern_src,
+        "kernel_ms": kernels[dom]["ms"],
+        "algorithmic_bytes_per_launch": kernels[dom]["bytes_per_frame"] * n_env,
+        "kernels": kernels,
+        "step": {"ms": k_ms, "algorithmic_bytes_per_frame": algorithmic_bytes(cfg),
+                 "achieved_gbs": step_gbs, "frac": step_gbs / peak},
+        # pyramid FMAs of a dense frame (zero columns are skipped, so "dense
+        # equivalent"): over the whole step and over the blur kernel alone
+        "fp32_fma": {"per_frame_dense": fma,
+                     "achieved_tflops_dense_equiv": 2 * fma * n_env / (k_ms / 1e3) / 1e12,
+                     "blur_kernel_tflops_dense_equiv": 2 * fma * n_env / (kernels[BLUR]["ms"] / 1e3) / 1e12
+                     if BLUR in kernels else None,
+                     "peak_tflops": 2 * fma_peak / 1e12},
     }
+    line["gpu_launches"] = a.steps * launches
+    line["clocks"] = clocks
+    line["device"] = props.name
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not a.no_cpu_baseline:
         cores = host_cores()
-        arm = CpuArm(a.config, a.seed, cores)
+        arm = CpuArm(a, cores)
         fpc = max(2, int(a.cpu_seconds / arm.per_frame))
         agg, per_core, wall, frames = arm.step(fpc)
         arm.close()
         line["cpu_baseline"] = {
-            "value": agg, "unit": UNIT, "cores": cores, "kind": "port",
-            "per_core": per_core,
-            "sample": f"{frames} frames ({cores}x{fpc}) of configs[{a.config}], oracle port "
-                      f"(REF/tactile.py:219 scipy blur + numpy gradient/LUT/markers), f64, {wall:.1f} s wall",
+            "value": agg, "unit": UNIT, "cores": cores, "kind": "port", "per_core": per_core,
+            "sample": arm.describe(a, fpc) + f"; {frames} frames in {wall:.1f} s wall",
         }
     print(json.dumps(line), flush=True)
 
 
+def relaunch(a):
+    """bench.py --gpus N outside torchrun: start N ranks of this script."""
+    import socket
+    import subprocess
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(relaunch(a))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if a.impl == "reference":
         run_reference(a, rank, world)
         return

@@ -143,19 +143,20 @@ int32_t tac_tiles_per_frame(const tac_ctx* ctx);
 int32_t tac_pipeline_path(const tac_ctx* ctx);
 /* Diagnostics: number of kernel launches one tac_pipeline call makes for n_env. */
 int32_t tac_pipeline_launches(const tac_ctx* ctx, int64_t n_env);
-/* Diagnostics: runs tac_pipeline `iters` times with a CUDA event pair around
- * every kernel launch (synchronising the stream after each) and writes the
- * mean per-call milliseconds of each kernel kind: kernel_ms[0] = blur (or the
- * fused frame kernel), [1] = shade, [2] = per-env epilogue (0 when absent). */
+/* Diagnostics: per-kernel timing.  kernel_ms has TAC_TIMING_KINDS slots:
+ * [0] = blur (or the fused frame kernel), [1] = shade, [2] = per-env
+ * epilogue, [3] = shadow march (0 when a kind does not run). */
+#define TAC_TIMING_KINDS 4
+/* Runs tac_pipeline `iters` times inside a timing session (below) and writes
+ * the mean per-call milliseconds of each kernel kind. */
 int tac_pipeline_profile(const tac_ctx* ctx, const tac_pipeline_args* args, void* stream,
                          int32_t iters, float* kernel_ms);
-/* Diagnostics: between tac_timing_begin and tac_timing_end, the first
- * max_calls single-chunk band-path tac_pipeline calls on this context record
- * CUDA events at their kernel boundaries on the call's stream (no
- * synchronisation, so a timed loop runs unchanged).  tac_timing_end waits for
- * the last event and writes the mean per-call milliseconds of [blur, shade,
- * epilogue] and the number of calls recorded (0: none; e.g. the fused path).
- * Not thread-safe while timing is on. */
+/* Between tac_timing_begin and tac_timing_end, the first max_calls
+ * tac_pipeline calls on this context record CUDA events at their kernel
+ * boundaries on the call's stream (no synchronisation, so a timed loop runs
+ * unchanged).  tac_timing_end waits for the last event and writes the mean
+ * per-call milliseconds of each kind (summed over a call's env chunks) and
+ * the number of calls recorded.  One session per context at a time. */
 int tac_timing_begin(const tac_ctx* ctx, int32_t max_calls);
 int tac_timing_end(const tac_ctx* ctx, float* kernel_ms, int32_t* calls);
 

@@ -33,11 +33,13 @@ struct tac_ctx {
   long long chunk5;                  // envs per v5 launch pair
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
-  // diagnostics: boundary events of the pipeline calls between
-  // tac_timing_begin and tac_timing_end (not thread-safe while on)
+  // diagnostics: kernel-boundary events of the pipeline calls between
+  // tac_timing_begin and tac_timing_end (one session per context)
   mutable struct {
     std::vector<cudaEvent_t> ev;
-    int cap = 0, used = 0;
+    std::vector<int> kind;
+    std::vector<std::pair<int, int>> calls;  // [first event, count) of each recorded call
+    int next = 0, max_calls = 0;
     bool on = false;
   } timing;
 };
@@ -613,7 +615,7 @@ int tac_shadow(const tac_ctx* c, const float* in, int32_t input_kind, float* fac
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_shadow");
 }
 
-static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream, float* kt) {
+int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   if (!a) return fail(TAC_ERR_INVALID, "null args");
   if (a->struct_size != sizeof(tac_pipeline_args))
     return fail(TAC_ERR_INVALID, "tac_pipeline_args.struct_size is %u, this library expects %zu",
@@ -653,39 +655,31 @@ static int run_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stre
   p.disp = a->disp;
   p.splat = a->splat;
   p.shadow = a->shadow;
+  // diagnostics timeline (tac_timing_begin .. tac_timing_end)
+  Marks tm;
+  auto& tg = c->timing;
+  if (tg.on && (int)tg.calls.size() < tg.max_calls && tg.next < (int)tg.ev.size()) {
+    tm.ev = tg.ev.data() + tg.next;
+    tm.kind = tg.kind.data() + tg.next;
+    tm.cap = (int)tg.ev.size() - tg.next;
+    tm.s = (cudaStream_t)stream;
+  }
   cudaError_t e;
   if (v5) {
     bind_workspace5(c, p, a->workspace, a->n_env);
-    cudaEvent_t* ev4 = nullptr;
-    auto& tg = c->timing;
-    if (tg.on && !kt && tg.used < tg.cap && (c->chunk5 <= 0 || a->n_env <= c->chunk5))
-      ev4 = tg.ev.data() + 4 * tg.used++;
-    e = launch_frame5(p, (cudaStream_t)stream, kt, ev4);
+    e = launch_frame5(p, (cudaStream_t)stream, &tm);
   } else {
     e = bind_workspace(c, p, a->workspace, a->n_env, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "tac_pipeline");
-    cudaEvent_t t0 = nullptr, t1 = nullptr;
-    if (kt) {
-      cudaEventCreate(&t0);
-      cudaEventCreate(&t1);
-      cudaEventRecord(t0, (cudaStream_t)stream);
-    }
+    tm.start();
     e = launch_frame(p, kModeFused, (cudaStream_t)stream);
-    if (kt) {
-      cudaEventRecord(t1, (cudaStream_t)stream);
-      cudaEventSynchronize(t1);
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, t0, t1);
-      kt[0] += ms;
-      cudaEventDestroy(t0);
-      cudaEventDestroy(t1);
-    }
+    tm.mark(0);
+  }
+  if (tm.on() && tm.n > 1) {
+    tg.calls.emplace_back(tg.next, tm.n);
+    tg.next += tm.n;
   }
   return e == cudaSuccess ? TAC_OK : cuda_fail(e, "tac_pipeline");
-}
-
-int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
-  return run_pipeline(c, a, stream, nullptr);
 }
 
 int32_t tac_pipeline_path(const tac_ctx* c) {
@@ -710,14 +704,18 @@ int tac_timing_begin(const tac_ctx* c, int32_t max_calls) {
   int st = check_device(c);
   if (st) return st;
   auto& tg = c->timing;
-  while ((int)tg.ev.size() < 4 * max_calls) {
+  // room for 2 launches per env chunk + 4 per call (shadow, epilogue, start)
+  const size_t want = (size_t)max_calls * 24;
+  while (tg.ev.size() < want) {
     cudaEvent_t e;
     cudaError_t r = cudaEventCreate(&e);
     if (r != cudaSuccess) return cuda_fail(r, "cudaEventCreate");
     tg.ev.push_back(e);
   }
-  tg.cap = max_calls;
-  tg.used = 0;
+  tg.kind.assign(tg.ev.size(), -1);
+  tg.calls.clear();
+  tg.next = 0;
+  tg.max_calls = max_calls;
   tg.on = true;
   return TAC_OK;
 }
@@ -726,34 +724,39 @@ int tac_timing_end(const tac_ctx* c, float* kernel_ms, int32_t* calls) {
   if (!c || !kernel_ms || !calls) return fail(TAC_ERR_INVALID, "null argument");
   auto& tg = c->timing;
   tg.on = false;
-  for (int k = 0; k < 3; ++k) kernel_ms[k] = 0.f;
-  *calls = tg.used;
-  if (tg.used == 0) return TAC_OK;
-  cudaError_t r = cudaEventSynchronize(tg.ev[4 * tg.used - 1]);
+  for (int k = 0; k < kTimingKinds; ++k) kernel_ms[k] = 0.f;
+  *calls = (int32_t)tg.calls.size();
+  if (tg.calls.empty()) return TAC_OK;
+  cudaError_t r = cudaEventSynchronize(tg.ev[tg.next - 1]);
   if (r != cudaSuccess) return cuda_fail(r, "cudaEventSynchronize");
-  double sum[3] = {0, 0, 0};
-  for (int i = 0; i < tg.used; ++i)
-    for (int k = 0; k < 3; ++k) {
+  double sum[kTimingKinds] = {0, 0, 0, 0};
+  for (const auto& cl : tg.calls)
+    for (int i = cl.first + 1; i < cl.first + cl.second; ++i) {
       float ms = 0.f;
-      r = cudaEventElapsedTime(&ms, tg.ev[4 * i + k], tg.ev[4 * i + k + 1]);
+      r = cudaEventElapsedTime(&ms, tg.ev[i - 1], tg.ev[i]);
       if (r != cudaSuccess) return cuda_fail(r, "cudaEventElapsedTime");
-      sum[k] += ms;
+      if (tg.kind[i] >= 0 && tg.kind[i] < kTimingKinds) sum[tg.kind[i]] += ms;
     }
-  for (int k = 0; k < 3; ++k) kernel_ms[k] = (float)(sum[k] / tg.used);
-  tg.used = 0;  // reported once
+  for (int k = 0; k < kTimingKinds; ++k) kernel_ms[k] = (float)(sum[k] / tg.calls.size());
+  tg.calls.clear();  // reported once
+  tg.next = 0;
   return TAC_OK;
 }
 
 int tac_pipeline_profile(const tac_ctx* c, const tac_pipeline_args* a, void* stream, int32_t iters,
                          float* kernel_ms) {
   if (!kernel_ms || iters < 1) return fail(TAC_ERR_INVALID, "kernel_ms and iters >= 1 are required");
-  float kt[3] = {0.f, 0.f, 0.f};
+  int st = tac_timing_begin(c, iters);
+  if (st) return st;
   for (int i = 0; i < iters; ++i) {
-    const int st = run_pipeline(c, a, stream, kt);
-    if (st) return st;
+    st = tac_pipeline(c, a, stream);
+    if (st) {
+      c->timing.on = false;
+      return st;
+    }
   }
-  for (int k = 0; k < 3; ++k) kernel_ms[k] = kt[k] / iters;
-  return TAC_OK;
+  int32_t n = 0;
+  return tac_timing_end(c, kernel_ms, &n);
 }
 
 }  // extern "C"

@@ -594,35 +594,7 @@ int frame5_launches(const FrameParams& p, long long n_env) {
   return (int)(2 * ((n_env + chunk - 1) / chunk) + (p.finalize != 0 ? 1 : 0));
 }
 
-// event-timed launch (diagnostics): kt[kind] += elapsed ms
-struct KTimer {
-  float* kt;
-  cudaStream_t s;
-  cudaEvent_t a = nullptr, b = nullptr;
-  KTimer(float* k, cudaStream_t st) : kt(k), s(st) {
-    if (kt) {
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
-    }
-  }
-  ~KTimer() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
-  }
-  void start() {
-    if (kt) cudaEventRecord(a, s);
-  }
-  void stop(int kind) {
-    if (!kt) return;
-    cudaEventRecord(b, s);
-    cudaEventSynchronize(b);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, a, b);
-    kt[kind] += ms;
-  }
-};
-
-cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt, cudaEvent_t* ev4) {
+cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm) {
   const size_t smem = band_blur_smem_bytes(p0);
   cudaError_t e = cudaFuncSetAttribute(band_blur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -635,11 +607,9 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt, cuda
   const unsigned nq = (unsigned)((p0.H + rpc - 1) / rpc);
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
   const long long nchunks = (p0.n_env + chunk - 1) / chunk;
-  KTimer tm(kt, s);
-  // in-stream boundary events (no synchronisation): before blur, after blur,
-  // after shade, after the epilogue; single-chunk calls only
-  if (nchunks != 1) ev4 = nullptr;
-  if (ev4) cudaEventRecord(ev4[0], s);
+  Marks none;
+  if (!tm) tm = &none;
+  tm->start();
 #define CK(x)                          \
   do {                                 \
     e = (x);                           \
@@ -656,25 +626,19 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, float* kt, cuda
     p.partials = p0.partials + e0 * p0.bands * kSumFields;
     if (p0.shadow) p.shadow = p0.shadow + e0 * HW;
     p.n_env = n;
-    tm.start();
     band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
     CK(cudaGetLastError());
-    tm.stop(0);
-    if (ev4) cudaEventRecord(ev4[1], s);
-    tm.start();
+    tm->mark(0);
     band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
     CK(cudaGetLastError());
-    tm.stop(1);
-    if (ev4) cudaEventRecord(ev4[2], s);
+    tm->mark(1);
   }
 #undef CK
   if (p0.finalize != 0) {
-    tm.start();
     env_epilogue_kernel<<<(unsigned)p0.n_env, 128, 0, s>>>(p0);
     e = cudaGetLastError();
-    tm.stop(2);
+    tm->mark(2);
   }
-  if (ev4) cudaEventRecord(ev4[3], s);
   return e;
 }
 

@@ -103,6 +103,32 @@ struct FrameParams {
   float* scratch;        // workspace [chunk][H][W] blurred (or the caller's blurred output)
 };
 
+// In-stream kernel-boundary events of one tac_pipeline call (diagnostics):
+// start() before the first launch, mark(kind) after each launch; the time
+// between consecutive events is charged to the kind of the later one.  Kinds:
+// 0 = blur (or a fused frame kernel), 1 = shade, 2 = per-env epilogue,
+// 3 = shadow march.  No synchronisation: a timed loop runs unchanged.
+constexpr int kTimingKinds = 4;
+struct Marks {
+  cudaEvent_t* ev = nullptr;  // pool slots [0, cap)
+  int* kind = nullptr;
+  int cap = 0, n = 0;
+  cudaStream_t s = nullptr;
+  bool on() const { return ev != nullptr; }
+  void start() { put(-1); }
+  void mark(int k) { put(k); }
+  void put(int k) {
+    if (!ev) return;
+    if (n >= cap) {  // out of slots: this call is dropped (tac_timing_end counts complete calls)
+      ev = nullptr;
+      n = -1;
+      return;
+    }
+    cudaEventRecord(ev[n], s);
+    kind[n++] = k;
+  }
+};
+
 // add_shadows march tables (REF/optical.py:283-299), built on the host.
 struct ShadowParams {
   int H, W;
@@ -125,9 +151,7 @@ size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 // band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
 bool frame5_eligible(const FrameParams& p);
-// kt (nullable, diagnostics): accumulates the CUDA-event time of each kernel
-// kind [blur, shade, epilogue] in ms (synchronises the stream per launch).
-cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, float* kt = nullptr, cudaEvent_t* ev4 = nullptr);
+cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, Marks* tm = nullptr);
 int frame5_launches(const FrameParams& p, long long n_env);
 int frame5_vpitch(int W, int R4);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,

@@ -163,14 +163,27 @@ class TactilePipeline:
         _lib.check(self.ctx.lib.tac_pipeline(self.ctx.handle, ctypes.byref(args), self.ctx.stream()),
                    "tac_pipeline")
 
+    def path(self):
+        """TAC_PATH_* tac_pipeline takes for aligned input (diagnostics)."""
+        return int(self.ctx.lib.tac_pipeline_path(self.ctx.handle))
+
+    def path_name(self):
+        return {_lib.TAC_PATH_BAND: "band", _lib.TAC_PATH_FUSED: "fused"}.get(self.path(), "?")
+
+    def kernel_names(self):
+        """Kernel of each timing slot [blur, shade, epilogue] of this path."""
+        if self.path() == _lib.TAC_PATH_FUSED:
+            return ["frame_kernel (fused)"]
+        return ["band_blur_kernel", "band_shade_kernel", "env_epilogue_kernel"]
+
     def launches_per_call(self, n_env):
         """Kernel launches one tac_pipeline call makes (diagnostics)."""
         return int(self.ctx.lib.tac_pipeline_launches(self.ctx.handle, int(n_env)))
 
     def profile(self, args, iters=10):
         """Mean per-call CUDA-event milliseconds of each kernel kind
-        [blur (or the fused frame kernel), shade, per-env epilogue]."""
-        ms = (ctypes.c_float * 3)()
+        [blur (or the fused frame kernel), shade, per-env epilogue, shadow]."""
+        ms = (ctypes.c_float * _lib.TAC_TIMING_KINDS)()
         _lib.check(self.ctx.lib.tac_pipeline_profile(self.ctx.handle, ctypes.byref(args), self.ctx.stream(),
                                                      int(iters), ms), "tac_pipeline_profile")
         return [float(v) for v in ms]
@@ -181,8 +194,8 @@ class TactilePipeline:
         _lib.check(self.ctx.lib.tac_timing_begin(self.ctx.handle, int(max_calls)), "tac_timing_begin")
 
     def timing_end(self):
-        """(mean per-call ms of [blur, shade, epilogue], calls recorded)."""
-        ms = (ctypes.c_float * 3)()
+        """(mean per-call ms of [blur, shade, epilogue, shadow], calls recorded)."""
+        ms = (ctypes.c_float * _lib.TAC_TIMING_KINDS)()
         calls = ctypes.c_int32(0)
         _lib.check(self.ctx.lib.tac_timing_end(self.ctx.handle, ms, ctypes.byref(calls)), "tac_timing_end")
         return [float(v) for v in ms], int(calls.value)

@@ -36,3 +36,22 @@ def gather_summaries(local: torch.Tensor, out: torch.Tensor = None, group=None, 
                           device=local.device)
     work = dist.all_gather_into_tensor(out, local.contiguous(), group=group, async_op=async_op)
     return (out, work) if async_op else out
+
+
+def gather_env_summaries(local: torch.Tensor, n_total: int, group=None):
+    """All-gather per-env [n_local, 8] summaries of contiguous ``env_block``
+    shards into the global [n_total, 8] in env order.  Ragged splits are
+    padded to ``ceil(n_total / world)`` rows for ``all_gather_into_tensor``
+    and stripped afterwards (bench.py keeps padded buffers resident instead)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    blk = -(-int(n_total) // world)
+    s, e = env_block(rank, world, n_total)
+    if local.shape[0] != e - s:
+        raise ValueError(f"rank {rank} holds {local.shape[0]} envs, env_block says {e - s}")
+    pad = torch.zeros((blk,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: e - s] = local
+    full = gather_summaries(pad, group=group)
+    parts = [full[r * blk: r * blk + (env_block(r, world, n_total)[1] - env_block(r, world, n_total)[0])]
+             for r in range(world)]
+    return torch.cat(parts, 0)

@@ -35,6 +35,10 @@ class IndenterParams:
     perm: np.ndarray  # [N, 256] Perlin permutation
     off: np.ndarray  # [N, 2] Perlin lattice offset
 
+    def subset(self, idx):
+        """The indenters of the given env indices (a slice or an index array)."""
+        return IndenterParams(*(getattr(self, f)[idx] for f in ("kind", "pen", "cx", "cy", "yaw", "perm", "off")))
+
 
 def indenters(n, h, w, seed, *, kinds=KINDS, pen=(0.0, 1.2e-3), pitch=PITCH, fixed_kind=None):
     rng = np.random.default_rng(seed)
@@ -167,3 +171,17 @@ def baseline_config(index, seed=0):
         dot_radius=3,
     )
     return cfg, n
+
+
+def workload(index, seed=0, n_total=None):
+    """The seeded global workload of configs[index]: (cfg, n_total, indenter
+    params of every env, shear [n,2], twist [n]).  Env e has the same frame
+    and load whatever the GPU count, so ranks slice it with
+    ``sharding.env_block`` (strong scaling) and the CPU baseline samples it."""
+    cfg, n = baseline_config(index, seed)
+    if n_total:
+        n = int(n_total)
+    h, w = cfg.sensor.image_size
+    params = indenters(n, h, w, seed + 10)
+    shear, twist = loads(n, seed + 20)
+    return cfg, n, params, shear, twist

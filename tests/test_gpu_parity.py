@@ -699,7 +699,7 @@ class TestDiagnostics:
         args = pipe.launch_args(depth, torch.as_tensor(shear, device=DEV), torch.as_tensor(twist, device=DEV), out)
         assert pipe.launches_per_call(n) == 3  # band blur, band shade, per-env epilogue
         ms = pipe.profile(args, iters=2)
-        assert len(ms) == 3 and all(v > 0 for v in ms)
+        assert len(ms) == 4 and all(v > 0 for v in ms[:3]) and ms[3] == 0.0  # no shadow march
         # the profiled calls produce the same frame as a plain call
         rgb = out.rgb.clone()
         pipe.launch(args)
@@ -723,11 +723,28 @@ class TestDiagnostics:
         for _ in range(4):
             pipe.launch(args)
         ms, calls = pipe.timing_end()
-        assert calls == 3 and len(ms) == 3 and all(v > 0 for v in ms)
+        assert calls == 3 and len(ms) == 4 and all(v > 0 for v in ms[:3])
         torch.cuda.synchronize()
         assert torch.equal(out.rgb, rgb)
         ms, calls = pipe.timing_end()  # nothing recorded since
-        assert calls == 0 and ms == [0.0, 0.0, 0.0]
+        assert calls == 0 and ms == [0.0] * 4
+
+    def test_in_stream_timing_sums_env_chunks(self):
+        """A call split into several env chunks is recorded whole: its blur /
+        shade times are the sums over its chunks."""
+        cfg = dataclasses.replace(small_config(48, 64), chunk_envs=2)
+        pipe = TactilePipeline(cfg, DEV)
+        n = 5
+        depth = depth_batch(n, 48, 64, seed=77).to(DEV)
+        shear, twist = synthetic.loads(n, 78)
+        out = pipe.allocate(n)
+        args = pipe.launch_args(depth, torch.as_tensor(shear, device=DEV), torch.as_tensor(twist, device=DEV), out)
+        pipe.launch(args)
+        pipe.timing_begin(2)
+        pipe.launch(args)
+        pipe.launch(args)
+        ms, calls = pipe.timing_end()
+        assert calls == 2 and all(v > 0 for v in ms[:3])
 
     def test_cuda_graph_capture_replays_the_step(self):
         """The whole tac_pipeline call (all its launches) can be captured in a

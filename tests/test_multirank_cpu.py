@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2411_04776_b200.sharding import env_block, gather_summaries
+from paper_2411_04776_b200.sharding import env_block, gather_env_summaries, gather_summaries
 
 
 def _free_port():
@@ -46,7 +46,7 @@ def _worker(rank, world, port, n_total, q):
         depth = depth_batch(n_total, 24, 32, seed=5).numpy().astype(np.float64)
         s, e = env_block(rank, world, n_total)
         local = torch.as_tensor(_summaries(depth[s:e], synthetic.PITCH, synthetic.REST))
-        full = gather_summaries(local)
+        full = gather_env_summaries(local, n_total) if n_total % world else gather_summaries(local)
         q.put((rank, full.numpy()))
     finally:
         dist.destroy_process_group()
@@ -63,7 +63,8 @@ def test_env_block_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_gloo_world2_gather_matches_single_process():
+@pytest.mark.parametrize("n_total", [8, 7])
+def test_gloo_world2_gather_matches_single_process(n_total):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -72,7 +73,6 @@ def test_gloo_world2_gather_matches_single_process():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    n_total = 8
     procs = [ctx.Process(target=_worker, args=(r, 2, port, n_total, q)) for r in range(2)]
     env = dict(os.environ)
     os.environ["PYTHONPATH"] = os.pathsep.join([here, os.path.dirname(here), env.get("PYTHONPATH", "")])
