@@ -71,9 +71,11 @@ enum {
 
 /* Kernel selection for tac_pipeline (tac_config.kernel_path). */
 enum {
-  TAC_PATH_AUTO = 0,  /* fastest eligible path (see tac_pipeline_path) */
-  TAC_PATH_BAND = 1,  /* round-1 band-tiled blur + band shade (W <= 320, R <= 16) */
-  TAC_PATH_FUSED = 2  /* strip-streaming fused frame kernel (any shape) */
+  TAC_PATH_AUTO = 0,   /* fastest eligible path (see tac_pipeline_path) */
+  TAC_PATH_BAND = 1,   /* band-tiled blur + band shade (W <= 320, R <= 16) */
+  TAC_PATH_FUSED = 2,  /* strip-streaming fused frame kernel (any shape) */
+  TAC_PATH_STREAM = 3  /* row-streaming blur + band shade (W % 16 == 0, the pyramids
+                          tac_stream.cu is instantiated for) */
 };
 
 /* Load sources for the marker stage of tac_pipeline. */

@@ -31,6 +31,7 @@ TAC_LUT_F16 = 1
 TAC_PATH_AUTO = 0
 TAC_PATH_BAND = 1
 TAC_PATH_FUSED = 2
+TAC_PATH_STREAM = 3
 TAC_TIMING_KINDS = 4
 
 _p = ctypes.c_void_p

@@ -131,7 +131,7 @@ class PipelineConfig:
     # execution choices (tac_config.lut_dtype / kernel_path / chunk_envs):
     # lut_dtype "f16" stores the LUT coefficients in fp16 (half the shade
     # kernel's gather bytes, <= 2^-11 relative per coefficient); kernel_path
-    # "auto" | "band" | "fused" picks the tac_pipeline kernels (A/B and tests)
+    # "auto" | "stream" | "band" | "fused" picks the tac_pipeline kernels (A/B and tests)
     lut_dtype: str = "f32"
     kernel_path: str = "auto"
     chunk_envs: int = 0
@@ -169,8 +169,8 @@ class PipelineConfig:
         object.__setattr__(self, "light_dirs", dirs)
         if self.lut_dtype not in ("f32", "f16"):
             raise InvalidArgumentError("lut_dtype must be 'f32' or 'f16'")
-        if self.kernel_path not in ("auto", "band", "fused"):
-            raise InvalidArgumentError("kernel_path must be 'auto', 'band' or 'fused'")
+        if self.kernel_path not in ("auto", "stream", "band", "fused"):
+            raise InvalidArgumentError("kernel_path must be 'auto', 'stream', 'band' or 'fused'")
         if int(self.chunk_envs) < 0:
             raise InvalidArgumentError("chunk_envs must be >= 0")
 

@@ -89,7 +89,7 @@ class Context:
         c.shadow_softness = float(cfg.shadow_softness)
         c.lut_dtype = {"f32": _lib.TAC_LUT_F32, "f16": _lib.TAC_LUT_F16}[cfg.lut_dtype]
         c.kernel_path = {"auto": _lib.TAC_PATH_AUTO, "band": _lib.TAC_PATH_BAND,
-                         "fused": _lib.TAC_PATH_FUSED}[cfg.kernel_path]
+                         "fused": _lib.TAC_PATH_FUSED, "stream": _lib.TAC_PATH_STREAM}[cfg.kernel_path]
         c.chunk_envs = int(cfg.chunk_envs)
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):

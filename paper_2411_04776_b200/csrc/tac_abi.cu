@@ -28,9 +28,10 @@ struct tac_ctx {
   float* d_shadow_cost = nullptr;
   ShadowParams shadow;
   FrameParams fused, blur, contact;  // per-mode launch templates
-  FrameParams fused5;                // band-tiled two-kernel geometry (default)
-  bool use5;
-  long long chunk5;                  // envs per v5 launch pair
+  FrameParams fused5;                // two-kernel geometry (row-streaming or band-tiled blur)
+  bool use5;                         // two-kernel path (TAC_PATH_STREAM or TAC_PATH_BAND)
+  int path;                          // TAC_PATH_* taken for aligned input
+  long long chunk5;                  // envs per blur/shade launch pair
   MarkerGeom mg;
   int max_tiles;  // max column strips per frame over the modes
   // diagnostics: kernel-boundary events of the pipeline calls between
@@ -113,8 +114,8 @@ size_t v5_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   if (!c->use5) return 0;
   const long long C = std::min<long long>(n_env, c->chunk5);
   const FrameParams& p = c->fused5;
-  return align256((size_t)n_env * p.bands * kSumFields * sizeof(double)) +
-         align256((size_t)C * p.bands * sizeof(int2)) + align256((size_t)C * p.H * p.W * sizeof(float));
+  return align256((size_t)n_env * p.nparts * kSumFields * sizeof(double)) +
+         align256((size_t)C * p.bands * p.ext_strips * sizeof(int2)) + align256((size_t)C * p.H * p.W * sizeof(float));
 }
 
 size_t v3_workspace_bytes(const tac_ctx* c, int64_t n_env) {
@@ -126,9 +127,9 @@ void bind_workspace5(const tac_ctx* c, FrameParams& p, void* ws, int64_t n_env) 
   const long long C = std::min<long long>(n_env, c->chunk5);
   char* b = reinterpret_cast<char*>(ws) + v3_workspace_bytes(c, n_env);
   p.partials = reinterpret_cast<double*>(b);
-  b += align256((size_t)n_env * p.bands * kSumFields * sizeof(double));
+  b += align256((size_t)n_env * p.nparts * kSumFields * sizeof(double));
   p.band_ext = reinterpret_cast<int2*>(b);
-  b += align256((size_t)C * p.bands * sizeof(int2));
+  b += align256((size_t)C * p.bands * p.ext_strips * sizeof(int2));
   p.scratch = reinterpret_cast<float*>(b);
   p.chunk = C;
 }
@@ -220,7 +221,7 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   if (k.dot_radius < 0 || k.dot_radius > 32) return fail(TAC_ERR_UNSUPPORTED, "dot_radius must be in 0..32");
   if (k.lut_dtype != TAC_LUT_F32 && k.lut_dtype != TAC_LUT_F16)
     return fail(TAC_ERR_INVALID, "unknown lut_dtype %d", k.lut_dtype);
-  if (k.kernel_path < TAC_PATH_AUTO || k.kernel_path > TAC_PATH_FUSED)
+  if (k.kernel_path < TAC_PATH_AUTO || k.kernel_path > TAC_PATH_STREAM)
     return fail(TAC_ERR_INVALID, "unknown kernel_path %d", k.kernel_path);
   if (k.chunk_envs < 0) return fail(TAC_ERR_INVALID, "chunk_envs must be >= 0");
   if (k.lut_dtype == TAC_LUT_F16) return fail(TAC_ERR_UNSUPPORTED, "lut_dtype f16 is not available in this build");
@@ -407,10 +408,8 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
     for (int i = 0; i <= r; ++i) {
       b.wv[l][i] = (float)w[i];
       b.wh[l][i] = (float)(w[i] / k.n_levels);
-      if (i <= 16) {
-        b.wv2[l][i] = make_float2(b.wv[l][i], b.wv[l][i]);
-        b.wh2[l][i] = make_float2(b.wh[l][i], b.wh[l][i]);
-      }
+      b.wv2[l][i] = make_float2(b.wv[l][i], b.wv[l][i]);
+      b.wh2[l][i] = make_float2(b.wh[l][i], b.wh[l][i]);
     }
   }
   b.rest = (float)k.gel_thickness;
@@ -455,9 +454,32 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   c->contact = b;
   plan_strips(c->contact, kModeContact, max_strip);
   c->max_tiles = std::max({c->fused.strips, c->blur.strips, c->contact.strips});
+  // tac_pipeline path: row-streaming blur (instantiated pyramids) > band blur
+  // (W <= 320, R <= 16) > strip-streaming fused kernel (anything else)
   c->fused5 = c->fused;
   plan_v5(c->fused5);
-  c->use5 = k.kernel_path != TAC_PATH_FUSED && frame5_eligible(c->fused5);
+  c->fused5.nparts = c->fused5.bands;
+  c->fused5.ext_strips = 1;
+  c->fused5.st_kind = -1;
+  c->path = TAC_PATH_FUSED;
+  {
+    FrameParams st = c->fused5;
+    plan_stream(st);
+    const bool want = k.kernel_path == TAC_PATH_AUTO || k.kernel_path == TAC_PATH_STREAM;
+    if (want && st.st_kind >= 0 && shade5_eligible(st)) {
+      st.nparts = st.st_strips;
+      st.ext_strips = st.st_strips;
+      c->fused5 = st;
+      c->path = TAC_PATH_STREAM;
+    } else if ((k.kernel_path == TAC_PATH_AUTO || k.kernel_path == TAC_PATH_BAND) && frame5_eligible(c->fused5)) {
+      c->path = TAC_PATH_BAND;
+    }
+  }
+  if (k.kernel_path != TAC_PATH_AUTO && c->path != k.kernel_path) {
+    free_ctx(c);
+    return fail(TAC_ERR_UNSUPPORTED, "kernel_path %d is not available for this configuration", k.kernel_path);
+  }
+  c->use5 = c->path == TAC_PATH_STREAM || c->path == TAC_PATH_BAND;
   c->chunk5 = k.chunk_envs > 0 ? k.chunk_envs : 4096;
   for (int mode = 0; mode < 3; ++mode) {
     FrameParams& p = mode == kModeFused ? c->fused : (mode == kModeBlur ? c->blur : c->contact);
@@ -684,7 +706,7 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
 
 int32_t tac_pipeline_path(const tac_ctx* c) {
   if (!c) return -1;
-  return c->use5 ? TAC_PATH_BAND : TAC_PATH_FUSED;
+  return c->path;
 }
 
 int32_t tac_pipeline_launches(const tac_ctx* c, int64_t n_env) {

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     ha = 16 * k_lo;
     hb = 16 * k_hi + 15;
   }
-  if (tid == 0) p.band_ext[env * nb + band] = make_int2(ha, hb);
+  if (tid == 0) p.band_ext[env * nb + band] = make_int2(ha, hb);  // ext_strips == 1
   // H items: row pair m x 8 columns; lanes 0..7 = row pairs of one chunk
   const int m = tid & 7;
   const int k8 = tid >> 3;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(K1T, TAC_K1_MINB) band_blur_kernel(const __gri
     t[4] = fmax(t[4], s_red[w * 8 + 4]);
     t[5] += s_red[w * 8 + 5];
   }
-  double* q = p.partials + (env * nb + band) * kSumFields;
+  double* q = p.partials + (env * p.nparts + band) * kSumFields;  // nparts == bands
   for (int i = 0; i < 6; ++i) q[i] = t[i];
 }
 
@@ -478,11 +478,18 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   const float* rc = p.scratch + env * HW + (long long)yc * W + xg;
   uint8_t* out = p.rgb + env * HW * 3;
 
-  // columns whose gradient can be non-zero: band extents of rows y-1..y+1, +-1
-  const int2* ext = p.band_ext + env * p.bands;
-  const int2 e0 = __ldg(ext + (max(yc - 1, 0) >> 4));
-  const int2 e1 = __ldg(ext + (min(yc + 1, H - 1) >> 4));
-  const int sa = min(e0.x, e1.x), sb = max(e0.y, e1.y);
+  // columns whose gradient can be non-zero: band extents of rows y-1..y+1
+  // (union over the blur kernel's column strips), +-1
+  const int ns = p.ext_strips;
+  const int2* ext = p.band_ext + env * p.bands * ns;
+  const int ba = max(yc - 1, 0) >> 4, bb = min(yc + 1, H - 1) >> 4;
+  int sa = INT_MAX, sb = INT_MIN;
+  for (int s = 0; s < ns; ++s) {
+    const int2 e0 = __ldg(ext + ba * ns + s);
+    const int2 e1 = __ldg(ext + bb * ns + s);
+    sa = min(sa, min(e0.x, e1.x));
+    sb = max(sb, max(e0.y, e1.y));
+  }
   // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
   const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
   float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant
   __shared__ double s_dbl[8];
   __shared__ int s_int[2 * 1024];
   const long long env = blockIdx.x;
-  const int nb = p.bands;
+  const int nb = p.nparts;
   if (threadIdx.x < 32) {
     // warp 0: lane s folds bands s, s + 32, ...; then a fixed xor butterfly
     // (every lane ends with the same bits: deterministic for a given band count)
@@ -588,6 +595,14 @@ bool frame5_eligible(const FrameParams& p) {
   return band_blur_smem_bytes(p) <= 227 * 1024;
 }
 
+// The band shade kernel and the epilogue behind the row-streaming blur.
+bool shade5_eligible(const FrameParams& p) {
+  if (p.W % 16 != 0 || p.W < 16) return false;
+  if (p.mg.rows * p.mg.cols > 1024) return false;
+  if (p.lut_tex == 0) return false;
+  return shade_rows_per_cta(p.W / 4) != 0;
+}
+
 int frame5_launches(const FrameParams& p, long long n_env) {
   if (n_env == 0) return 0;
   const long long chunk = p.chunk > 0 ? p.chunk : n_env;
@@ -623,11 +638,15 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm) {
     p.in = p0.in + e0 * HW;
     p.rgb = p0.rgb + e0 * HW * 3;
     p.scratch = p0.blurred ? p0.blurred + e0 * HW : p0.scratch;
-    p.partials = p0.partials + e0 * p0.bands * kSumFields;
+    p.partials = p0.partials + e0 * p0.nparts * kSumFields;
     if (p0.shadow) p.shadow = p0.shadow + e0 * HW;
     p.n_env = n;
-    band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
-    CK(cudaGetLastError());
+    if (p.st_kind >= 0) {
+      CK(launch_stream_blur(p, s));
+    } else {
+      band_blur_kernel<<<dim3((unsigned)p.bands, (unsigned)n), b1, smem, s>>>(p);
+      CK(cudaGetLastError());
+    }
     tm->mark(0);
     band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
     CK(cudaGetLastError());

@@ -55,8 +55,8 @@ struct FrameParams {
   int radius[TAC_MAX_LEVELS];
   float wv[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // vertical taps, centre first
   float wh[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // horizontal taps, folded with 1/L
-  float2 wv2[TAC_MAX_LEVELS][17];                // (w, w) pairs of wv / wh for FFMA2 (radius <= 16)
-  float2 wh2[TAC_MAX_LEVELS][17];
+  float2 wv2[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];  // (w, w) pairs of wv / wh for FFMA2
+  float2 wh2[TAC_MAX_LEVELS][TAC_MAX_RADIUS + 1];
   // clamp / contact
   float rest;            // gel thickness rounded to fp32
   float rest_lo;         // rest - (double)rest: the clamp runs in ~fp64 accuracy
@@ -99,8 +99,16 @@ struct FrameParams {
   // band-tiled two-kernel path (tac_frame5.cu)
   int bands;             // ceil(H / 16)
   long long chunk;       // envs per (blur, shade) launch pair
-  int2* band_ext;        // workspace [chunk][bands] blurred non-zero column range
+  int2* band_ext;        // workspace [chunk][bands][ext_strips] blurred non-zero column range
   float* scratch;        // workspace [chunk][H][W] blurred (or the caller's blurred output)
+  int ext_strips;        // band_ext entries per band (column strips of the blur kernel)
+  int nparts;            // contact partials per env (reduced by env_epilogue_kernel)
+  // row-streaming blur (tac_stream.cu)
+  int st_kind;           // pyramid instantiation (stream_kind); -1 = not eligible
+  int st_strips;         // column strips per frame (CTAs per env)
+  int st_ip;             // input slot row pitch (floats)
+  int st_rpp;            // V buffer row-pair pitch (floats)
+  int st_nvw, st_nhw;    // V / H warps per CTA
 };
 
 // In-stream kernel-boundary events of one tac_pipeline call (diagnostics):
@@ -151,7 +159,14 @@ size_t frame_smem_bytes(const FrameParams& p);
 cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 // band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
 bool frame5_eligible(const FrameParams& p);
+bool shade5_eligible(const FrameParams& p);
 cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, Marks* tm = nullptr);
+// row-streaming path (tac_stream.cu): plan (sets st_* / -1 when not
+// eligible), smem bytes, and the blur launch of one env chunk.
+void plan_stream(FrameParams& p);
+size_t stream_smem_bytes(const FrameParams& p);
+cudaError_t launch_stream_blur(const FrameParams& p, cudaStream_t s);
+
 int frame5_launches(const FrameParams& p, long long n_env);
 int frame5_vpitch(int W, int R4);
 cudaError_t launch_indentation(const float* depth, float* ind, float rest, float rest_lo, long long n,

@@ -168,13 +168,16 @@ class TactilePipeline:
         return int(self.ctx.lib.tac_pipeline_path(self.ctx.handle))
 
     def path_name(self):
-        return {_lib.TAC_PATH_BAND: "band", _lib.TAC_PATH_FUSED: "fused"}.get(self.path(), "?")
+        return {_lib.TAC_PATH_BAND: "band", _lib.TAC_PATH_FUSED: "fused",
+                _lib.TAC_PATH_STREAM: "stream"}.get(self.path(), "?")
 
     def kernel_names(self):
         """Kernel of each timing slot [blur, shade, epilogue] of this path."""
-        if self.path() == _lib.TAC_PATH_FUSED:
+        path = self.path()
+        if path == _lib.TAC_PATH_FUSED:
             return ["frame_kernel (fused)"]
-        return ["band_blur_kernel", "band_shade_kernel", "env_epilogue_kernel"]
+        blur = "stream_blur_kernel" if path == _lib.TAC_PATH_STREAM else "band_blur_kernel"
+        return [blur, "band_shade_kernel", "env_epilogue_kernel"]
 
     def launches_per_call(self, n_env):
         """Kernel launches one tac_pipeline call makes (diagnostics)."""
