@@ -417,6 +417,8 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   b.threshold = (float)k.contact_threshold;
   b.half_w = 0.5f * k.width;
   b.half_h = 0.5f * k.height;
+  b.xoff = 0.5 - 0.5 * k.width;
+  b.yoff = 0.5 - 0.5 * k.height;
   b.inv_p = (float)(1.0 / k.pixel_pitch);
   b.inv_2p = (float)(1.0 / (2.0 * k.pixel_pitch));
   b.mag_scale = (float)(k.mag_bins / k.g_max);

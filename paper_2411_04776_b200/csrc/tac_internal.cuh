@@ -62,6 +62,7 @@ struct FrameParams {
   float rest_lo;         // rest - (double)rest: the clamp runs in ~fp64 accuracy
   float threshold;
   float half_w, half_h;  // W/2, H/2 (pixel-centre coordinates)
+  double xoff, yoff;     // 0.5 - W/2, 0.5 - H/2: pixel-centre coordinate of column / row 0
   // shading
   float inv_p, inv_2p;
   float mag_scale;       // mag_bins / g_max

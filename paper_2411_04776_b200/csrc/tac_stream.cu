@@ -1,33 +1,37 @@
-// Row-streaming, warp-specialised blur (kernel (a), default tac_pipeline path).
+// Row-streaming, warp-specialised blur (kernel (a) of the default tac_pipeline path).
 //
 // indentation_from + smooth_pyramid (REF/tactile.py:193-222) + the contact
 // partials of contact_center (REF/marker.py:103-121) for one env column strip
-// per CTA, walking down the frame in blocks of SB = 8 rows:
+// (<= 320 output columns) per CTA, walking down the frame in blocks of SB = 8
+// rows:
 //
-//   TMA      one elected thread streams 8-row input blocks into NS_IN smem
-//            slots with cp.async.bulk (mbarrier complete_tx), NS_IN - 1
-//            blocks ahead of the vertical pass.
+//   TMA      thread 0 streams 8-row input blocks into NS smem slots with
+//            cp.async.bulk (mbarrier complete_tx), NS - 1 blocks ahead.
 //   V warps  one lane per column pair.  Every input row is read from smem
 //            ONCE, clamped (REF/tactile.py:195-196), folded into the contact
-//            partials, and pushed into a register ring of the last P rows;
-//            the vertical pass of EVERY level is then evaluated from the ring
-//            with pair sums shared by the levels, w0 x[y] + sum_t w_t (x[y+t]
-//            + x[y-t]): R_max FADD2 + sum_l (R_l + 1) FFMA2 per output row
-//            pair of columns (36 instead of 45 for sigma 1,2,4).  Outputs go
-//            to a double-buffered smem block [level][row pair][column] with
-//            rows interleaved in pairs, plus a per-row-pair bitmask of the
-//            column pairs that are non-zero.  Replicate borders: rows
-//            outside the frame are copies of the edge row (ring fill), the
-//            edge column lanes write the column pads.
-//   H warps  one (row pair, 8 columns) item per lane: every FFMA2 operand is
-//            one aligned float2 of the interleaved block (LDS.128), summed
-//            over the levels in registers, written to HBM with 16-B stores.
-//            Items whose window is all zero (bitmask) store exact zeros.
+//            partials and pushed into a register ring of the last P rows.
+//            Per output row pair the vertical pass of EVERY level is
+//            evaluated from the ring with pair sums shared by the levels,
+//            w0 x[y] + sum_t w_t (x[y+t] + x[y-t]): R_max FADD2 +
+//            sum_l (R_l + 1) FFMA2 per output row of a column pair (36
+//            instead of 45 for sigma 1,2,4), both rows of a pair sharing each
+//            uniform-register tap load.  Outputs go to a double-buffered smem
+//            block [level][row pair][column] with rows interleaved in pairs,
+//            plus a per-row-pair bitmask of the non-zero column pairs.
+//            Replicate borders: rows outside the frame are copies of the
+//            edge row (ring fill); the warp holding an edge column writes the
+//            column pads cooperatively (one float4 per lane).
+//   H warps  one (row pair, 8 columns) item per lane and block, <= 2 items
+//            per lane: the item's window of each level is loaded into
+//            registers (LDS.128, every FFMA2 operand one aligned float2 of
+//            the interleaved block) and convolved tap-outer, summed over the
+//            levels, stored to HBM with 16-B stores.  Items whose window is
+//            all zero (bitmask) store exact zeros.
 //
 // V and H warps hand blocks over with named barriers (FULL[s] / EMPTY[s],
 // s = block parity); nothing else synchronises the CTA inside the loop.  The
-// pyramid radii are template parameters (stream_kind), so every ring index,
-// smem slot and tap is static: the inner loops are straight-line FFMA2.
+// pyramid radii and the smem pitches are template parameters, so every ring
+// index, smem offset and tap is static.
 #include <climits>
 
 #include "tac_frame_common.cuh"
@@ -36,13 +40,13 @@ namespace tac {
 
 namespace {
 
-constexpr int SB = 8;          // rows per stream block
-constexpr int kMaxVW = 8;      // V warps per CTA (<= 512 columns per strip)
-constexpr int kStreamMaxT = 384;
+constexpr int SB = 8;           // rows per stream block
+constexpr int kMaxVW = 8;       // V warps per CTA
+constexpr int kMaxStrip = 320;  // output columns per CTA
 
 // barrier ids (0 = __syncthreads)
-constexpr int kBarFull = 1;    // + slot
-constexpr int kBarEmpty = 3;   // + slot
+constexpr int kBarFull = 1;   // + block parity
+constexpr int kBarEmpty = 3;  // + block parity
 constexpr int kBarV = 5;
 constexpr int kBarH = 6;
 
@@ -54,23 +58,36 @@ struct Pyr {
   static constexpr int cmax(int a, int b) { return a > b ? a : b; }
   static constexpr int R = cmax(cmax(R0, L_ > 1 ? R1 : 0), cmax(L_ > 2 ? R2 : 0, L_ > 3 ? R3 : 0));
   static constexpr int R4 = (R + 3) & ~3;
-  static constexpr int P = (2 * R + 1 + SB - 1) / SB * SB;  // ring rows (multiple of SB)
-  static constexpr int NS = P / SB;                          // input slots: slot pattern repeats every P rows
-  // two CTAs per SM (<= 102 registers) when the ring is short enough
-  // (8 warps = 4 per SMSP: <= 128 registers per thread for the V ring)
-  static constexpr int MINB = P <= 32 && L <= 3 ? 2 : 1;
-  static constexpr int MAXT = MINB == 2 ? 256 : kStreamMaxT;
+  static constexpr int P = 2 * R + SB;                      // ring rows: an iteration's 8 outputs need 2R + 8
+  static constexpr int NS = 4;                              // input slots: an iteration reads 2 blocks, + 2 ahead
+  // 8 warps (4 per SMSP at 2 CTAs/SM: 128 registers) when the ring is short
+  static constexpr int MINB = (P <= 32 && L <= 3) ? 2 : 1;
+  static constexpr int MAXT = MINB == 2 ? 256 : 384;
 };
 
-// stream_kind -> radii (host and device agree through this table)
-using Pyr0 = Pyr<3, 3, 6, 12>;        // sigma 1, 2, 4 (BASELINE configs[0-2, 4])
-using Pyr1 = Pyr<4, 3, 6, 12, 24>;    // sigma 1, 2, 4, 8 (configs[3])
-using Pyr2 = Pyr<4, 2, 5, 10, 15>;    // kernel sizes 5, 11, 21, 31 (REF DEFAULT_PYRAMID)
-using Pyr3 = Pyr<3, 0, 2, 5>;         // kernel sizes 1, 5, 11
-constexpr int kStreamKinds = 4;
+using Pyr0 = Pyr<3, 3, 6, 12>;      // sigma 1, 2, 4 (BASELINE configs[0-2, 4])
+using Pyr1 = Pyr<4, 3, 6, 12, 24>;  // sigma 1, 2, 4, 8 (configs[3])
+using Pyr2 = Pyr<4, 2, 5, 10, 15>;  // kernel sizes 5, 11, 21, 31 (REF DEFAULT_PYRAMID)
+using Pyr3 = Pyr<3, 0, 2, 5>;       // kernel sizes 1, 5, 11
 
-template <class PY>
-struct KindOf;
+// Compile-time smem geometry of one instantiation: WIDE = frames split into
+// column strips (V range = strip + R4 halo columns each side).
+template <class PY, bool WIDE>
+struct Geo5 {
+  static constexpr int IP = (WIDE ? kMaxStrip + 2 * PY::R4 : kMaxStrip);  // input slot row (floats)
+  static constexpr int VP0 = IP + 2 * PY::R4;                             // V row: pads + range
+  static constexpr int VP = ((VP0 / 2) & 1) ? VP0 : VP0 + 2;              // row-pair pitch 2 VP = 4 x odd
+  static constexpr int RPP = 2 * VP;                                      // floats per row pair
+  static constexpr int VSLOT = PY::L * (SB / 2) * RPP;                    // floats per V block slot
+  static constexpr size_t IN_OFF = 0;
+  static constexpr size_t VB_OFF = ((size_t)PY::NS * SB * IP * 4 + 127) & ~size_t(127);
+  static constexpr size_t NZ_OFF = VB_OFF + (size_t)2 * VSLOT * 4;
+  static constexpr size_t RED_OFF = NZ_OFF + (size_t)2 * (SB / 2) * kMaxVW * 4;
+  static constexpr size_t BAR_OFF = RED_OFF + (size_t)kMaxVW * 8 * 8;
+  static constexpr size_t EXT_OFF = BAR_OFF + (size_t)PY::NS * 8;
+  // + nbands * nhw int2 (runtime)
+  static size_t bytes(int nbands, int nhw) { return (EXT_OFF + (size_t)nbands * nhw * 8 + 127) & ~size_t(127); }
+};
 
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   float2 r;
@@ -88,45 +105,15 @@ __device__ __forceinline__ void bar_arrive_n(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Shared-memory carve-up (dynamic smem), identical on host and device.
-struct StreamSmem {
-  size_t in_off, vb_off, nz_off, ext_off, red_off, bar_off, total;
-};
-
-__host__ __device__ inline StreamSmem stream_smem(int L, int NS, int ip, int rpp, int nbands, int nhw) {
-  StreamSmem s;
-  size_t o = 0;
-  s.in_off = o;
-  o += (size_t)NS * SB * ip * sizeof(float);
-  o = (o + 127) & ~size_t(127);
-  s.vb_off = o;
-  o += (size_t)2 * L * (SB / 2) * rpp * sizeof(float);
-  s.nz_off = o;
-  o += (size_t)2 * (SB / 2) * kMaxVW * sizeof(uint32_t);
-  s.ext_off = o;
-  o += (size_t)nbands * nhw * sizeof(int2);
-  o = (o + 7) & ~size_t(7);
-  s.red_off = o;
-  o += (size_t)kMaxVW * 8 * sizeof(double);
-  s.bar_off = o;
-  o += (size_t)NS * sizeof(uint64_t);
-  s.total = (o + 127) & ~size_t(127);
-  return s;
-}
-
-// One H item: row pair m x 8 columns of a block (acc[i] = (row 2m, row 2m+1)
-// at column c0 + i).  Returns false (acc = 0) when the V window of the widest
-// level is all zero, or for a lane without an item.
-template <class PY>
-__device__ __forceinline__ bool h_item(const FrameParams& p, const float* vslot, const uint32_t* nzb, int item,
-                                       int nitems, int x0, int vx0, int npairs, float2 (&acc)[8]) {
+// One H item: row pair m x 8 columns (acc[i] = (row 2m, row 2m+1) at column
+// c0 + i) from the V block slot `vs` (column index 0 = global column vx0 - R4).
+// Returns false (acc = 0) when the V window of the widest level is all zero.
+template <class PY, class G>
+__device__ __forceinline__ bool h_item(const FrameParams& p, const float* vs, const uint32_t* nzs, int m, int c0,
+                                       int vx0, int npairs, float2 (&acc)[8]) {
   constexpr int L = PY::L, R4 = PY::R4;
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
-  if (item >= nitems) return false;
-  const int m = item & 3;
-  const int c0 = x0 + 8 * (item >> 2);
-  const uint32_t* nzs = nzb + m * kMaxVW;
   const int qa = max((c0 - R4 - vx0) >> 1, 0);
   const int qb = min((c0 + 8 + R4 - vx0) >> 1, npairs) - 1;
   bool any = false;
@@ -138,56 +125,61 @@ __device__ __forceinline__ bool h_item(const FrameParams& p, const float* vslot,
     any |= bits != 0u;
   }
   if (!any) return false;
-  const int rpp = p.st_rpp;
+  // row pair m at column c0 - R4 (16-B aligned: every offset is a multiple of 4 columns)
+  const float* base = vs + m * G::RPP + 2 * (c0 - vx0);
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     const int rl_ = PY::r(l), r4l = PY::r4(l);
-    // row pair m of level l from column c0 - r4l (16-B aligned: every offset is a multiple of 4 columns)
-    const float* src_l = vslot + (size_t)(l * (SB / 2) + m) * rpp + 2 * (c0 - r4l - vx0 + R4);
-    // the window 2 columns at a time: window column cc feeds output i with tap cc - r4l - i
+    float2 v[8 + 2 * PY::R4];
 #pragma unroll
-    for (int qq = 0; qq < (8 + 2 * r4l) / 2; ++qq) {
-      const float4 f = *reinterpret_cast<const float4*>(src_l + 4 * qq);
-      const float2 va = make_float2(f.x, f.y), vbb = make_float2(f.z, f.w);
+    for (int q = 0; q < (8 + 2 * r4l) / 2; ++q) {
+      const float4 f = *reinterpret_cast<const float4*>(base + l * (SB / 2) * G::RPP + 2 * (R4 - r4l) + 4 * q);
+      v[2 * q] = make_float2(f.x, f.y);
+      v[2 * q + 1] = make_float2(f.z, f.w);
+    }
+    // tap-outer: each uniform-register tap serves the 8 outputs
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int cc = 2 * qq + h;
+    for (int t = -rl_; t <= rl_; ++t) {
+      const float ws = p.wh[l][t < 0 ? -t : t];
+      const float2 w = make_float2(ws, ws);  // scalar uniform operand (FFMA2 .F32 broadcast)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int t = cc - r4l - i;
-          if (t >= -rl_ && t <= rl_) acc[i] = ffma2(p.wh2[l][t < 0 ? -t : t], h ? vbb : va, acc[i]);
-        }
-      }
+      for (int i = 0; i < 8; ++i) acc[i] = ffma2(w, v[r4l + i + t], acc[i]);
     }
   }
   return true;
 }
 
-__device__ __forceinline__ void h_store(const FrameParams& p, long long env, long long HW, int W, int H, int y0,
-                                        int x0, int item, int nitems, const float2 (&acc)[8], bool any, int& lo,
-                                        int& hi) {
-  if (item >= nitems) return;
-  const int m = item & 3;
-  const int c0 = x0 + 8 * (item >> 2);
-  const int y = y0 + 2 * m;
-  float* d = p.scratch + env * HW + (long long)y * W + c0;
-  if (y < H) {
-    reinterpret_cast<float4*>(d)[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
-    reinterpret_cast<float4*>(d)[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);
-  }
-  if (y + 1 < H) {
-    reinterpret_cast<float4*>(d + W)[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
-    reinterpret_cast<float4*>(d + W)[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
-  }
-  if (any) {
-    lo = min(lo, c0);
-    hi = max(hi, c0 + 7);
+// Input block b (rows 8b..8b+7, columns [vx0, vx0 + ncols)) -> smem slot
+// `dst` with bulk copies completing on `bar`.  Rows past the frame bottom are
+// copies of row H-1 (replicate border, REF/tactile.py:220 mode="nearest").
+// One thread; out of line: it runs once per block.
+__device__ __forceinline__ void stream_issue(const float* src, float* dst, uint64_t* bar, int b, int ip, int H, int W,
+                                          int vx0, int ncols) {
+  const unsigned rbytes = (unsigned)ncols * 4u;
+  mbar_expect_tx(bar, rbytes * (unsigned)SB);
+  const float* g = src + vx0;
+  if (ncols == W && W == ip && SB * b + SB <= H) {
+    bulk_g2s(dst, g + (long long)SB * b * W, rbytes * (unsigned)SB, bar);  // contiguous rows
+  } else {
+    for (int i = 0; i < SB; ++i) bulk_g2s(dst + i * ip, g + (long long)min(SB * b + i, H - 1) * W, rbytes, bar);
   }
 }
 
+// Blocks [next, lim) into their slots (block b -> slot b % ns); returns lim.
+__device__ __forceinline__ int stream_refill(const float* src, float* in_s, uint64_t* s_full, int next, int lim, int ns,
+                                          int ip, int H, int W, int vx0, int ncols) {
+#pragma unroll 1
+  for (; next < lim; ++next) {
+    const int slot = next % ns;
+    stream_issue(src, in_s + slot * SB * ip, &s_full[slot], next, ip, H, W, vx0, ncols);
+  }
+  return next;
+}
+
 // ---------------------------------------------------------------------------
-template <class PY>
+template <class PY, bool WIDE>
 __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const __grid_constant__ FrameParams p) {
+  using G = Geo5<PY, WIDE>;
   constexpr int L = PY::L, R = PY::R, R4 = PY::R4, P = PY::P, NS = PY::NS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const long long env = blockIdx.x;
@@ -198,40 +190,26 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
   const int x1 = min(x0 + p.strip_w, W);
   const int vx0 = max(x0 - R4, 0);
   const int vx1 = min(x1 + R4, W);
-  const int ip = p.st_ip, rpp = p.st_rpp;
   const int nvw = p.st_nvw, nhw = p.st_nhw;
   const int nthreads = 32 * (nvw + nhw);
   const int nbands = (H + 15) >> 4;
-  const int nblk = (H + SB - 1) / SB;  // output (and input) blocks
-  const StreamSmem sm = stream_smem(L, NS, ip, rpp, nbands, nhw);
-  float* in_s = reinterpret_cast<float*>(smem_raw + sm.in_off);
-  float* vb = reinterpret_cast<float*>(smem_raw + sm.vb_off);
-  uint32_t* s_nz = reinterpret_cast<uint32_t*>(smem_raw + sm.nz_off);
-  int2* s_ext = reinterpret_cast<int2*>(smem_raw + sm.ext_off);
-  double* s_red = reinterpret_cast<double*>(smem_raw + sm.red_off);
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(smem_raw + sm.bar_off);
+  const int nblk = (H + SB - 1) / SB;       // output blocks
+  // input blocks: the last iteration reads rows up to 8 nblk - 1 + R (copies of row H-1 past the frame)
+  const int nblk_in = nblk + (R + SB - 1) / SB;
+  float* in_s = reinterpret_cast<float*>(smem_raw + G::IN_OFF);
+  float* vb = reinterpret_cast<float*>(smem_raw + G::VB_OFF);
+  uint32_t* s_nz = reinterpret_cast<uint32_t*>(smem_raw + G::NZ_OFF);
+  double* s_red = reinterpret_cast<double*>(smem_raw + G::RED_OFF);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(smem_raw + G::BAR_OFF);
+  int2* s_ext = reinterpret_cast<int2*>(smem_raw + G::EXT_OFF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* src = p.in + env * HW;
-  const unsigned rbytes = (unsigned)(vx1 - vx0) * 4u;
 
-  // one thread streams input block b (rows 8b..) into slot b % NS
-  auto issue = [&](int b) {
-    const int slot = b % NS;
-    const int rows = min(SB, H - b * SB);
-    mbar_expect_tx(&s_full[slot], rbytes * (unsigned)rows);
-    float* dst = in_s + slot * SB * ip;
-    const float* g = src + (long long)b * SB * W + vx0;
-    if (vx0 == 0 && vx1 == W && ip == W) {
-      bulk_g2s(dst, g, rbytes * (unsigned)rows, &s_full[slot]);  // contiguous rows
-    } else {
-      for (int i = 0; i < rows; ++i) bulk_g2s(dst + i * ip, g + (long long)i * W, rbytes, &s_full[slot]);
-    }
-  };
+  // thread 0 streams input block b (rows 8b..8b+7) into slot b % NS
   if (threadIdx.x == 0) {
-    *reinterpret_cast<unsigned*>(s_red + kMaxVW * 8 - 1) = 0u;  // non-finite count
     for (int s = 0; s < NS; ++s) mbar_init(&s_full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int b = 0; b < NS && b < nblk; ++b) issue(b);
+    stream_refill(src, in_s, s_full, 0, min(NS, nblk_in), NS, G::IP, H, W, vx0, vx1 - vx0);
   }
   __syncthreads();
 
@@ -240,54 +218,57 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     const int q = warp * 32 + lane;  // column pair of the V range
     const int c = vx0 + 2 * q;
     const bool act = c < vx1;
-    const int cr = act ? c : vx1 - 2;              // inactive lanes read a valid column
-    const bool own = act && c >= x0 && c < x1;     // counted in this strip's contact partials
+    const int cr = act ? c : vx1 - 2;           // inactive lanes read a valid column
+    const bool own = act && c >= x0 && c < x1;  // counted in this strip's contact partials
     const float* col = in_s + (cr - vx0);
-    const bool padl = act && c == 0, padr = act && c + 2 == W;
-    // warp-uniform: only the warps holding a frame-edge column write pads
-    const bool pad_warp = __any_sync(0xffffffffu, padl || padr);
-    unsigned* s_nf = reinterpret_cast<unsigned*>(s_red + kMaxVW * 8 - 1);  // non-finite count (rare path)
+    float* vcol = vb + 2 * (c - vx0 + R4);  // the pair's float4 in row pair 0, level 0, slot 0
+    // the warps holding frame-edge columns write the column pads (warp-uniform)
+    const bool padl_w = vx0 == 0 && warp == 0;
+    const bool padr_w = vx1 == W && warp == (((W - 2 - vx0) >> 1) >> 5);
     const float2 rr = make_float2(p.rest, p.rest), rl = make_float2(p.rest_lo, p.rest_lo);
     const float thr = p.threshold;
     const bool depth_in = p.input_depth != 0;
-    const bool partials = p.finalize != 0;
+    const bool partials = p.finalize != 0 && own;
     const double yoff = 0.5 - (double)p.half_h;
     float cnt = 0.f, mx = 0.f;
-    float cs0 = 0.f, cs1 = 0.f;  // fp32 column sums of the current block (flushed to fp64 per block)
+    int nf = 0;
+    float cs0 = 0.f, cs1 = 0.f;  // fp32 column sums of the current input block
     double sw = 0.0, swx = 0.0, swy = 0.0;
     float2 win[P];
-    float2 last = make_float2(0.f, 0.f);
-    int last_nz = INT_MIN / 2;  // last input row with a non-zero value in this pair
+    int last_nz = INT_MIN / 2;  // last input row with a non-zero value in the warp's columns (warp-uniform)
 
-    // read + convert + fold one real row y (block already waited for)
-    auto take = [&](int y, int slot, int row) -> float2 {
-      const float2 raw = *reinterpret_cast<const float2*>(col + (slot * SB + row) * ip);
+    // read + convert one row y from smem slot / row; rows < H are folded into
+    // the contact partials (rows >= H are replicas of row H-1)
+    auto take = [&](int y, const float* src_row) -> float2 {
+      const float2 raw = *reinterpret_cast<const float2*>(src_row);
       float2 v = raw;
       if (depth_in) {
         v = fsubadd2(rr, raw, rl);
         v.x = clampf(v.x, 0.f, p.rest);
         v.y = clampf(v.y, 0.f, p.rest);
       }
-      if (own && partials) {
-        if (!(fabsf(raw.x + raw.y) < INFINITY))
-          atomicAdd(s_nf, (fabsf(raw.x) < INFINITY ? 0u : 1u) + (fabsf(raw.y) < INFINITY ? 0u : 1u));
-        mx = fmaxf(mx, fmaxf(v.x, v.y));
-        const float w0 = v.x > thr ? v.x : 0.f, w1 = v.y > thr ? v.y : 0.f;
-        cnt += (v.x > thr ? 1.f : 0.f) + (v.y > thr ? 1.f : 0.f);
-        cs0 += w0;
-        cs1 += w1;
-        const float rs = w0 + w1;
-        if (rs != 0.f) {
+      const bool nzw = __any_sync(0xffffffffu, (__float_as_uint(v.x) | __float_as_uint(v.y)) != 0u);
+      // raw non-finite values clamp to 0; count them (summary field 6)
+      if (!(fabsf(raw.x + raw.y) < INFINITY) && partials && y < H)
+        nf += (fabsf(raw.x) < INFINITY ? 0 : 1) + (fabsf(raw.y) < INFINITY ? 0 : 1);
+      if (nzw) {
+        last_nz = y;
+        if (partials && y < H) {
+          mx = fmaxf(mx, fmaxf(v.x, v.y));
+          const float w0 = v.x > thr ? v.x : 0.f, w1 = v.y > thr ? v.y : 0.f;
+          cnt += (v.x > thr ? 1.f : 0.f) + (v.y > thr ? 1.f : 0.f);
+          cs0 += w0;
+          cs1 += w1;
+          const float rs = w0 + w1;
           sw += (double)rs;
           swy = fma((double)rs, (double)y + yoff, swy);
         }
       }
-      if ((__float_as_uint(v.x) | __float_as_uint(v.y)) != 0u) last_nz = y;
       return v;
     };
     auto flush_cols = [&]() {
-      if (own && partials && (cs0 != 0.f || cs1 != 0.f)) {
-        const double xc0 = (double)c + 0.5 - (double)p.half_w;
+      if (partials && (cs0 != 0.f || cs1 != 0.f)) {
+        const double xc0 = (double)c + p.xoff;
         swx = fma((double)cs0, xc0, swx);
         swx = fma((double)cs1, xc0 + 1.0, swx);
       }
@@ -295,117 +276,103 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     };
 
     // ---- prologue: ring rows -R .. R-1 (rows < 0 replicate row 0) ----------
-    {
-      int waited = -1;
+    // ring layout at the start of iteration j: win[t] = row 8j - R + t, t < 2R
 #pragma unroll
-      for (int y = 0; y < R; ++y) {
-        if (y < H) {
-          const int b = y / SB;
-          if (b != waited) {
-            mbar_wait(&s_full[b % NS], (b / NS) & 1);
-            waited = b;
-          }
-          last = take(y, b % NS, y % SB);
-        }
-        win[(y % P + P) % P] = last;
-        if (y == 0) {
+    for (int y = 0; y < R; ++y) {
+      if (y % SB == 0) mbar_wait(&s_full[(y / SB) % NS], ((y / SB) / NS) & 1);
+      win[R + y] = take(y, col + ((y / SB) % NS * SB + y % SB) * G::IP);
+      if (y == 0) {
 #pragma unroll
-          for (int t = 1; t <= R; ++t) win[((-t) % P + P) % P] = last;
-        }
+        for (int t = 0; t < R; ++t) win[t] = win[R];
       }
-      flush_cols();
     }
+    flush_cols();
 
     // ---- main loop: iteration j = output rows 8j..8j+7 = input rows 8j+R.. ---
-    int j = 0;
-    int next_issue = min(NS, nblk);  // (thread 0) next input block to stream
-    for (int jj = 0; jj < nblk; jj += NS) {
+    // one iteration is unrolled; the ring shifts by 8 rows at its end
+#pragma unroll 1
+    for (int j = 0; j < nblk; ++j) {
+      const int sv = j & 1;
+      bar_sync_n(kBarEmpty + sv, nthreads);  // H finished block j-2; all V warps finished j-1
+      float* vs = vcol + sv * G::VSLOT;
+      uint32_t* nzs = s_nz + sv * (SB / 2) * kMaxVW + warp;
+      // input rows 8j+R+i live in blocks b0 = j + R/8 and b0 + 1
+      const int b0 = j + R / SB;
+      const float* blk0 = col + (b0 % NS) * SB * G::IP;
+      const float* blk1 = col + ((b0 + 1) % NS) * SB * G::IP;
 #pragma unroll
-      for (int u = 0; u < NS; ++u) {
-        j = jj + u;
-        if (j >= nblk) break;
-        const int sv = j & 1;
-        bar_sync_n(kBarEmpty + sv, nthreads);  // H finished block j-2; all V warps finished j-1
-        if (threadIdx.x == 0) {
-          // input blocks before the first one iteration j reads are free:
-          // refill their slots NS blocks ahead
-          const int lim = min((SB * j + R) / SB + NS, nblk);
-          while (next_issue < lim) issue(next_issue++);
-        }
-        float* vslot = vb + (size_t)sv * L * (SB / 2) * rpp;
-        uint32_t* nzs = s_nz + sv * (SB / 2) * kMaxVW;
-        float2 prev[L];
+      for (int k = 0; k < SB / 2; ++k) {
+        // push input rows yi = 8j + R + 2k, +1
 #pragma unroll
-        for (int l = 0; l < L; ++l) prev[l] = make_float2(0.f, 0.f);
-        bool prev_nz = false;
-#pragma unroll
-        for (int i = 0; i < SB; ++i) {
-          // input row yi = 8j + R + i  (static slot / ring index within the unrolled P rows)
+        for (int h = 0; h < 2; ++h) {
+          const int i = 2 * k + h;
+          const int rb = (R + i) / SB - R / SB;  // 0: block b0, 1: block b0 + 1
           const int yi = SB * j + R + i;
-          const int ring_in = (SB * u + R + i) % P;
-          const int slot_in = ring_in / SB;  // == (yi / SB) % NS since NS * SB == P
-          if (yi < H) {
-            if (i == 0 || ((R + i) % SB) == 0) mbar_wait(&s_full[slot_in], ((yi / SB) / NS) & 1);
-            last = take(yi, slot_in, (R + i) % SB);
-            if (((R + i) % SB) == SB - 1) flush_cols();
+          if (i == 0 || (R + i) % SB == 0) mbar_wait(&s_full[(b0 + rb) % NS], ((b0 + rb) / NS) & 1);
+          win[2 * R + i] = take(yi, (rb ? blk1 : blk0) + ((R + i) % SB) * G::IP);
+          if ((R + i) % SB == SB - 1) flush_cols();
+        }
+        // output rows yo = 8j + 2k (a) and yo + 1 (b): ring index R + 2k
+        const int ro = R + 2 * k;
+        float2 oa[L], ob[L];
+        if (last_nz >= SB * j + 2 * k - R) {  // warp-uniform: a non-zero row in the window
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            oa[l] = ffma2(make_float2(p.wv[l][0], p.wv[l][0]), win[ro], make_float2(0.f, 0.f));
+            ob[l] = ffma2(make_float2(p.wv[l][0], p.wv[l][0]), win[ro + 1], make_float2(0.f, 0.f));
           }
-          win[ring_in] = last;
-          // output row yo = 8j + i from ring rows yo-R .. yo+R
-          const int ro = (SB * u + i) % P;
-          float2 o[L];
-          const bool live = __any_sync(0xffffffffu, last_nz >= SB * j + i - R);
-          if (live) {
-            // w0 x[yo] + sum_t w_t (x[yo+t] + x[yo-t]): the pair sum of tap t is
-            // shared by every level with radius >= t
 #pragma unroll
-            for (int l = 0; l < L; ++l) o[l] = ffma2(p.wv2[l][0], win[ro], make_float2(0.f, 0.f));
+          for (int t = 1; t <= R; ++t) {
+            const float2 pa = fadd2(win[ro + t], win[ro - t]);
+            const float2 pb = fadd2(win[ro + 1 + t], win[ro + 1 - t]);
 #pragma unroll
-            for (int t = 1; t <= R; ++t) {
-              const float2 ps = fadd2(win[(ro + t) % P], win[(ro - t + P) % P]);
-#pragma unroll
-              for (int l = 0; l < L; ++l)
-                if (t <= PY::r(l)) o[l] = ffma2(p.wv2[l][t], ps, o[l]);
-            }
-          } else {
-#pragma unroll
-            for (int l = 0; l < L; ++l) o[l] = make_float2(0.f, 0.f);
-          }
-          bool nz = false;
-#pragma unroll
-          for (int l = 0; l < L; ++l) nz |= (__float_as_uint(o[l].x) | __float_as_uint(o[l].y)) != 0u;
-          if (i & 1) {
-            // row pair m = i/2: (rows 2m, 2m+1) x (columns c, c+1), one float4 per level
-            const int m = i >> 1;
-            if (act) {
-#pragma unroll
-              for (int l = 0; l < L; ++l) {
-                float* d = vslot + (size_t)(l * (SB / 2) + m) * rpp;
-                *reinterpret_cast<float4*>(d + 2 * (c - vx0 + R4)) =
-                    make_float4(prev[l].x, o[l].x, prev[l].y, o[l].y);
-                if (pad_warp && padl) {  // replicate columns -R4_l .. -1 (column 0)
-                  const float4 e4 = make_float4(prev[l].x, o[l].x, prev[l].x, o[l].x);
-#pragma unroll
-                  for (int k = 0; k < PY::r4(l); k += 2)
-                    *reinterpret_cast<float4*>(d + 2 * (R4 - PY::r4(l) + k)) = e4;
-                }
-                if (pad_warp && padr) {  // replicate columns W .. W+R4_l-1 (column W-1)
-                  const float4 e4 = make_float4(prev[l].y, o[l].y, prev[l].y, o[l].y);
-#pragma unroll
-                  for (int k = 0; k < PY::r4(l); k += 2)
-                    *reinterpret_cast<float4*>(d + 2 * (W - vx0 + R4 + k)) = e4;
-                }
+            for (int l = 0; l < L; ++l)
+              if (t <= PY::r(l)) {
+                oa[l] = ffma2(make_float2(p.wv[l][t], p.wv[l][t]), pa, oa[l]);
+                ob[l] = ffma2(make_float2(p.wv[l][t], p.wv[l][t]), pb, ob[l]);
               }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, act && (nz || prev_nz));
-            if (lane == 0) nzs[m * kMaxVW + warp] = bal;
-          } else {
+          }
+        } else {
 #pragma unroll
-            for (int l = 0; l < L; ++l) prev[l] = o[l];
-            prev_nz = nz;
+          for (int l = 0; l < L; ++l) oa[l] = ob[l] = make_float2(0.f, 0.f);
+        }
+        // the widest level's window contains every level's: non-negative
+        // inputs and positive taps make it zero only if all are
+        const bool nz = (__float_as_uint(oa[L - 1].x) | __float_as_uint(oa[L - 1].y) |
+                         __float_as_uint(ob[L - 1].x) | __float_as_uint(ob[L - 1].y)) != 0u;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          // rows (2k, 2k+1) x columns (c, c+1)
+          if (act)
+            *reinterpret_cast<float4*>(vs + (l * (SB / 2) + k) * G::RPP) =
+                make_float4(oa[l].x, ob[l].x, oa[l].y, ob[l].y);
+        }
+        if (padl_w || padr_w) {
+          // replicate pads: lane t < r4l/2 writes pad float4 t of each
+          // level from the edge column the warp just stored (column 0 /
+          // column W-1, read back after a warp barrier)
+          __syncwarp();
+          float* vrow = vb + sv * G::VSLOT + k * G::RPP;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            float* lrow = vrow + l * (SB / 2) * G::RPP;
+            if (padl_w && lane < PY::r4(l) / 2) {
+              const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * R4);
+              *reinterpret_cast<float4*>(lrow + 2 * (R4 - PY::r4(l) + 2 * lane)) = make_float4(e.x, e.y, e.x, e.y);
+            }
+            if (padr_w && lane < PY::r4(l) / 2) {
+              const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * (W - 1 - vx0 + R4));
+              *reinterpret_cast<float4*>(lrow + 2 * (W - vx0 + R4 + 2 * lane)) = make_float4(e.x, e.y, e.x, e.y);
+            }
           }
         }
-        bar_arrive_n(kBarFull + sv, nthreads);
+        const uint32_t bal = __ballot_sync(0xffffffffu, act && nz);
+        if (lane == 0) nzs[k * kMaxVW] = bal;
       }
+      bar_arrive_n(kBarFull + sv, nthreads);
+      // shift the ring by the 8 rows consumed
+#pragma unroll
+      for (int t = 0; t < 2 * R; ++t) win[t] = win[t + SB];
     }
     flush_cols();  // a partial last block
     // ---- contact partials of the strip: V warps only ----------------------------
@@ -413,7 +380,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     Red red;
     red.cnt = cnt;
     red.mx = mx;
-    red.nf = 0.f;
+    red.nf = (float)nf;
     red.sw = sw;
     red.swx = swx;
     red.swy = swy;
@@ -429,7 +396,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     }
     bar_sync_n(kBarV, 32 * nvw);
     if (threadIdx.x == 0) {
-      double t[6] = {0, 0, 0, 0, 0, (double)*s_nf};
+      double t[6] = {0, 0, 0, 0, 0, 0};
       for (int w = 0; w < nvw; ++w) {  // fixed order: deterministic
         for (int i = 0; i < 4; ++i) t[i] += s_red[w * 8 + i];
         t[4] = fmax(t[4], s_red[w * 8 + 4]);
@@ -440,26 +407,50 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     }
   } else {
     // ======================= H warps: horizontal pass + store ===================
-    // items = (row pair m, 8-column chunk) of a block; a lane takes items
-    // ht, ht + 32 nhw, ... (the same chunks in every block)
+    // items = (row pair m, 8-column chunk) of a block; lane ht takes items ht
+    // and ht + 32 nhw (the same chunks in every block)
     const int ht = threadIdx.x - 32 * nvw;
     const int hw = warp - nvw;
     const int nht = 32 * nhw;
     const int nitems = 4 * ((x1 - x0) >> 3);
     const int npairs = (vx1 - vx0) >> 1;
     int lo = INT_MAX, hi = INT_MIN;  // non-zero output columns of the current band
+    int next_issue = min(NS, nblk_in);  // (H thread 0) next input block to stream
     bar_arrive_n(kBarEmpty + 0, nthreads);
     if (nblk > 1) bar_arrive_n(kBarEmpty + 1, nthreads);
     for (int j = 0; j < nblk; ++j) {
       const int sv = j & 1;
       bar_sync_n(kBarFull + sv, nthreads);
-      const float* vslot = vb + (size_t)sv * L * (SB / 2) * rpp;
-      float2 acc0[8], acc1[8];
-      const bool any0 = h_item<PY>(p, vslot, s_nz + sv * (SB / 2) * kMaxVW, ht, nitems, x0, vx0, npairs, acc0);
-      const bool any1 = h_item<PY>(p, vslot, s_nz + sv * (SB / 2) * kMaxVW, ht + nht, nitems, x0, vx0, npairs, acc1);
+      if (ht == 0) {
+        // every V warp finished iteration j: the input blocks before the first
+        // one iteration j+1 reads are free; refill their slots NS blocks ahead
+        const int lim = min((SB * (j + 1) + R) / SB + NS, nblk_in);
+        if (next_issue < lim)
+          next_issue = stream_refill(src, in_s, s_full, next_issue, lim, NS, G::IP, H, W, vx0, vx1 - vx0);
+      }
+      const float* vs = vb + sv * G::VSLOT;
+#pragma unroll 1
+      for (int item = ht; item < nitems; item += nht) {
+        const int m = item & 3;
+        const int c0 = x0 + 8 * (item >> 2);
+        float2 acc[8];
+        const bool any = h_item<PY, G>(p, vs, s_nz + (sv * (SB / 2) + m) * kMaxVW, m, c0, vx0, npairs, acc);
+        const int y = SB * j + 2 * m;
+        float* d = p.scratch + env * HW + (long long)y * W + c0;
+        if (y < H) {
+          reinterpret_cast<float4*>(d)[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+          reinterpret_cast<float4*>(d)[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);
+        }
+        if (y + 1 < H) {
+          reinterpret_cast<float4*>(d + W)[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+          reinterpret_cast<float4*>(d + W)[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
+        }
+        if (any) {
+          lo = min(lo, c0);
+          hi = max(hi, c0 + 7);
+        }
+      }
       if (j + 2 < nblk) bar_arrive_n(kBarEmpty + sv, nthreads);
-      h_store(p, env, HW, W, H, SB * j, x0, ht, nitems, acc0, any0, lo, hi);
-      h_store(p, env, HW, W, H, SB * j, x0, ht + nht, nitems, acc1, any1, lo, hi);
       // band (16 rows = 2 blocks) complete: per-warp extent
       if ((j & 1) || j == nblk - 1) {
         const int blo = __reduce_min_sync(0xffffffffu, lo);
@@ -469,8 +460,8 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         hi = INT_MIN;
       }
     }
-    bar_sync_n(kBarH, 32 * nhw);
-    for (int b = ht; b < nbands; b += 32 * nhw) {
+    bar_sync_n(kBarH, nht);
+    for (int b = ht; b < nbands; b += nht) {
       int2 e = make_int2(INT_MAX, INT_MIN);
       for (int w = 0; w < nhw; ++w) {
         const int2 x = s_ext[b * nhw + w];
@@ -482,13 +473,16 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
   }
 }
 
-template <class PY>
+template <class PY, bool WIDE>
 cudaError_t launch_kind(const FrameParams& p, cudaStream_t s) {
-  const size_t smem = stream_smem_bytes(p);
-  cudaError_t e = cudaFuncSetAttribute(stream_blur_kernel<PY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  using G = Geo5<PY, WIDE>;
+  const size_t smem = G::bytes((p.H + 15) >> 4, p.st_nhw);
+  cudaError_t e = cudaFuncSetAttribute(stream_blur_kernel<PY, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
   if (p.n_env == 0) return cudaSuccess;
-  stream_blur_kernel<PY><<<dim3((unsigned)p.n_env, (unsigned)p.st_strips), 32 * (p.st_nvw + p.st_nhw), smem, s>>>(p);
+  stream_blur_kernel<PY, WIDE>
+      <<<dim3((unsigned)p.n_env, (unsigned)p.st_strips), 32 * (p.st_nvw + p.st_nhw), smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -500,67 +494,82 @@ bool kind_matches(const FrameParams& p) {
   return true;
 }
 
+// kind = 2 * pyramid + WIDE
 int stream_kind_of(const FrameParams& p) {
-  if (kind_matches<Pyr0>(p)) return 0;
-  if (kind_matches<Pyr1>(p)) return 1;
-  if (kind_matches<Pyr2>(p)) return 2;
-  if (kind_matches<Pyr3>(p)) return 3;
+  const int wide = p.W > kMaxStrip ? 1 : 0;
+  if (kind_matches<Pyr0>(p)) return 0 + wide;
+  if (kind_matches<Pyr1>(p)) return 2 + wide;
+  if (kind_matches<Pyr2>(p)) return 4 + wide;
+  if (kind_matches<Pyr3>(p)) return 6 + wide;
   return -1;
 }
 
-int kind_L(int k) { return k == 0 ? Pyr0::L : k == 1 ? Pyr1::L : k == 2 ? Pyr2::L : Pyr3::L; }
-int kind_R4(int k) { return k == 0 ? Pyr0::R4 : k == 1 ? Pyr1::R4 : k == 2 ? Pyr2::R4 : Pyr3::R4; }
-int kind_NS(int k) { return k == 0 ? Pyr0::NS : k == 1 ? Pyr1::NS : k == 2 ? Pyr2::NS : Pyr3::NS; }
+template <class PY>
+void kind_info(bool wide, int nbands, int nhw, int& r4, int& maxt, size_t& smem) {
+  r4 = PY::R4;
+  maxt = PY::MAXT;
+  smem = wide ? Geo5<PY, true>::bytes(nbands, nhw) : Geo5<PY, false>::bytes(nbands, nhw);
+}
+
+void kind_info(int k, int nbands, int nhw, int& r4, int& maxt, size_t& smem) {
+  const bool wide = k & 1;
+  switch (k >> 1) {
+    case 0: kind_info<Pyr0>(wide, nbands, nhw, r4, maxt, smem); break;
+    case 1: kind_info<Pyr1>(wide, nbands, nhw, r4, maxt, smem); break;
+    case 2: kind_info<Pyr2>(wide, nbands, nhw, r4, maxt, smem); break;
+    default: kind_info<Pyr3>(wide, nbands, nhw, r4, maxt, smem); break;
+  }
+}
 
 }  // namespace
 
 size_t stream_smem_bytes(const FrameParams& p) {
-  const int k = p.st_kind;
-  return stream_smem(kind_L(k), kind_NS(k), p.st_ip, p.st_rpp, (p.H + 15) >> 4, p.st_nhw).total;
+  int r4, maxt;
+  size_t smem;
+  kind_info(p.st_kind, (p.H + 15) >> 4, p.st_nhw, r4, maxt, smem);
+  return smem;
 }
 
 // Strips of <= 320 output columns (multiples of 16); V range = strip +- R4
-// columns clamped to the frame; one V lane per column pair, one H lane per
-// (row pair, 8 columns) of a 4-row-pair block.
+// columns clamped to the frame; one V lane per column pair, H lanes take
+// <= 2 (row pair, 8 columns) items per block.
 void plan_stream(FrameParams& p) {
   p.st_kind = -1;
   const int k = stream_kind_of(p);
   if (k < 0 || p.W % 16 != 0 || p.W < 16 || p.H < 1) return;
   if (p.mg.rows * p.mg.cols > 1024) return;  // epilogue scratch
-  const int R4 = kind_R4(k);
-  int strips = (p.W + 319) / 320;
+  int r4, maxt;
+  size_t smem;
+  kind_info(k, 1, 1, r4, maxt, smem);
+  int strips = (p.W + kMaxStrip - 1) / kMaxStrip;
   int sw = ((p.W + strips - 1) / strips + 15) & ~15;
   strips = (p.W + sw - 1) / sw;
-  const int vw = std::min(sw + 2 * R4, p.W);  // widest V range (columns)
+  const int vw = std::min(sw + 2 * r4, p.W);  // widest V range (columns)
   const int nvw = (vw / 2 + 31) / 32;
-  const int maxt = k == 0 ? Pyr0::MAXT : k == 1 ? Pyr1::MAXT : k == 2 ? Pyr2::MAXT : Pyr3::MAXT;
-  // H lanes take <= 2 (row pair, 8-column) items per block
   const int items = 4 * (sw / 8);
   int nhw = (items + 31) / 32;
   while (nhw > 1 && 32 * (nvw + nhw) > maxt) --nhw;
   if (nvw > kMaxVW || 32 * (nvw + nhw) > maxt || 2 * 32 * nhw < items) return;
   p.strip_w = sw;
   p.st_strips = strips;
-  p.st_ip = (vw + 3) & ~3;
-  int vp = p.st_ip + 2 * R4;  // floats per vb row: pads + V range
-  if (((vp / 2) & 1) == 0) vp += 2;  // row-pair pitch 2 vp = 4 x odd: conflict-free LDS.128 over 4 row pairs
-  p.st_rpp = 2 * vp;
   p.st_nvw = nvw;
   p.st_nhw = nhw;
+  p.st_ip = 0;
+  p.st_rpp = 0;
   p.st_kind = k;
   if (stream_smem_bytes(p) > 227 * 1024) p.st_kind = -1;
 }
 
 cudaError_t launch_stream_blur(const FrameParams& p, cudaStream_t s) {
   switch (p.st_kind) {
-    case 0:
-      return launch_kind<Pyr0>(p, s);
-    case 1:
-      return launch_kind<Pyr1>(p, s);
-    case 2:
-      return launch_kind<Pyr2>(p, s);
-    case 3:
-      return launch_kind<Pyr3>(p, s);
+    case 0: return launch_kind<Pyr0, false>(p, s);
+    case 1: return launch_kind<Pyr0, true>(p, s);
+    case 2: return launch_kind<Pyr1, false>(p, s);
+    case 3: return launch_kind<Pyr1, true>(p, s);
+    case 4: return launch_kind<Pyr2, false>(p, s);
+    case 5: return launch_kind<Pyr2, true>(p, s);
+    case 6: return launch_kind<Pyr3, false>(p, s);
+    case 7: return launch_kind<Pyr3, true>(p, s);
   }
   return cudaErrorInvalidValue;
 }
