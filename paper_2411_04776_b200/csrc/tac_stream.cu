@@ -60,7 +60,8 @@ struct Pyr {
   static constexpr int R4 = (R + 3) & ~3;
   static constexpr int P = 2 * R + SB;                      // ring rows: an iteration's 8 outputs need 2R + 8
   static constexpr int NS = 4;                              // input slots: an iteration reads 2 blocks, + 2 ahead
-  // 8 warps (4 per SMSP at 2 CTAs/SM: 128 registers) when the ring is short
+  // 8 warps (4 per SMSP at 2 CTAs/SM: <= 128 registers) when the ring is short;
+  // measured: 10 warps with a 96-register cap is 18 % slower
   static constexpr int MINB = (P <= 32 && L <= 3) ? 2 : 1;
   static constexpr int MAXT = MINB == 2 ? 256 : 384;
 };
