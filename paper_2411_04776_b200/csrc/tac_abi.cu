@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "tac_internal.cuh"
 
 using namespace tac;
@@ -20,6 +22,7 @@ struct tac_ctx {
   float4* d_lut = nullptr;
   float* d_bg = nullptr;
   float4* d_lut_half = nullptr;    // [2][bins][8] float: plane h = floats 8h..8h+7 of every bin (256-bit loads)
+  uint4* d_lut_h16 = nullptr;      // lut_dtype f16: [bins][16] fp16, direction-major (one 32-B sector per bin)
   cudaTextureObject_t lut_tex = 0;  // float4 texels over d_lut_half (texture path for the gathers)
   float* d_bg_planar = nullptr;    // [3][H*W]: R, G, B background planes (v5 shading)
   uint8_t* d_bg_u8 = nullptr;
@@ -140,6 +143,7 @@ int free_ctx(tac_ctx* c) {
   cudaFree(c->d_bg);
   if (c->lut_tex) cudaDestroyTextureObject(c->lut_tex);
   cudaFree(c->d_lut_half);
+  cudaFree(c->d_lut_h16);
   cudaFree(c->d_bg_planar);
   cudaFree(c->d_bg_u8);
   cudaFree(c->d_grid);
@@ -224,7 +228,6 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   if (k.kernel_path < TAC_PATH_AUTO || k.kernel_path > TAC_PATH_STREAM)
     return fail(TAC_ERR_INVALID, "unknown kernel_path %d", k.kernel_path);
   if (k.chunk_envs < 0) return fail(TAC_ERR_INVALID, "chunk_envs must be >= 0");
-  if (k.lut_dtype == TAC_LUT_F16) return fail(TAC_ERR_UNSUPPORTED, "lut_dtype f16 is not available in this build");
   if (k.n_lights < 0 || k.n_lights > TAC_MAX_LIGHTS)
     return fail(TAC_ERR_INVALID, "n_lights must be in 0..%d", TAC_MAX_LIGHTS);
   if (!(k.shadow_factor >= 0.0 && k.shadow_factor <= 1.0))
@@ -256,11 +259,23 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
     return cuda_fail(e, "cudaGetDevice");
   }
 
-  // LUT: [mag][dir][3][6] -> [mag*dir][16] = c1..c5 per channel + pad
+  // LUT: [mag][dir][3][6] -> [mag*dir][16] = c1..c5 per channel + pad.
+  // lut_dtype f16 rounds every coefficient to fp16 (nearest even) for ALL
+  // shading paths, so they compute with the same table
   std::vector<float> lut(nbins * 16, 0.f);
+  std::vector<__half> lut16(nbins * 16, __float2half_rn(0.f));
   for (size_t b = 0; b < nbins; ++b)
     for (int ch = 0; ch < 3; ++ch)
-      for (int t = 1; t < 6; ++t) lut[b * 16 + ch * 5 + (t - 1)] = k.lut[(b * 3 + ch) * 6 + t];
+      for (int t = 1; t < 6; ++t) {
+        float v = k.lut[(b * 3 + ch) * 6 + t];
+        if (k.lut_dtype == TAC_LUT_F16) {
+          const __half h = __float2half_rn(v);
+          v = __half2float(h);
+          const size_t mb = b / k.dir_bins, db = b % k.dir_bins;
+          lut16[(db * k.mag_bins + mb) * 16 + ch * 5 + (t - 1)] = h;
+        }
+        lut[b * 16 + ch * 5 + (t - 1)] = v;
+      }
   // half-planar LUT for the band shading kernel (plane h = floats 8h..8h+7 of
   // every bin, one 256-bit load each: a 128-B line holds 4 bins of a plane) and
   // R/G/B background planes (coalesced loads).  Bins in direction-major
@@ -306,8 +321,10 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
       {(void**)&c->d_lut_half, luth.data(), luth.size() * sizeof(float)},
       {(void**)&c->d_bg_planar, bgp.data(), bgp.size() * sizeof(float)},
       {(void**)&c->d_grid, grid.data(), grid.size() * sizeof(double)},
+      {(void**)&c->d_lut_h16, lut16.data(), k.lut_dtype == TAC_LUT_F16 ? lut16.size() * sizeof(__half) : 0},
   };
   for (auto& u : ups) {
+    if (u.bytes == 0) continue;
     e = cudaMalloc(u.dst, u.bytes);
     if (e == cudaSuccess) e = cudaMemcpy(*u.dst, u.src, u.bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -444,6 +461,7 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
   }
   b.lut_tex = c->lut_tex;
   b.bg_planar = c->d_bg_planar;
+  b.lut_h16 = c->d_lut_h16;
   b.nbins = (int)nbins_p;
   b.bg_u8 = c->d_bg_u8;
   b.mg = mg;

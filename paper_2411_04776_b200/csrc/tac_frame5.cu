@@ -41,6 +41,7 @@
 // Envs run in chunks of tac_config.chunk_envs (default 4096): smaller chunks keep the
 // blurred intermediate in L2 but measured slower (launch tails dominate).
 #include <climits>
+#include <cuda_fp16.h>
 #include <cstdio>
 #include <cstdlib>
 
@@ -359,6 +360,25 @@ __device__ __forceinline__ void ld256(const float* p, float4& a, float4& b) {
       : "l"(p));
 }
 
+// one 256-bit read-only load as 8 words (16 fp16 LUT coefficients)
+__device__ __forceinline__ void ld256u(const void* p, uint32_t (&w)[8]) {
+  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+      : "l"(p));
+}
+
+__device__ __forceinline__ float h2f_lo(uint32_t w) { return __half2float(__ushort_as_half((unsigned short)(w & 0xffffu))); }
+__device__ __forceinline__ float h2f_hi(uint32_t w) { return __half2float(__ushort_as_half((unsigned short)(w >> 16))); }
+
+// add_lut with the bin's 15 coefficients stored as fp16 (lut_dtype f16):
+// halfs [R c1..c5, G c1..c5, B c1..c5, pad], same operation order as add_lut
+__device__ __forceinline__ void add_lut_h(const uint32_t (&w)[8], float nx, float ny, float& r, float& g, float& b) {
+  const float nxx = nx * nx, nxy = nx * ny, nyy = ny * ny;
+  r += h2f_lo(w[0]) * nx + h2f_hi(w[0]) * ny + h2f_lo(w[1]) * nxx + h2f_hi(w[1]) * nxy + h2f_lo(w[2]) * nyy;
+  g += h2f_hi(w[2]) * nx + h2f_lo(w[3]) * ny + h2f_hi(w[3]) * nxx + h2f_lo(w[4]) * nxy + h2f_hi(w[4]) * nyy;
+  b += h2f_lo(w[5]) * nx + h2f_hi(w[5]) * ny + h2f_lo(w[6]) * nxx + h2f_hi(w[6]) * nxy + h2f_lo(w[7]) * nyy;
+}
+
 __device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) {
   return db * p.mag_bins + mb;  // direction-major (tac_ctx_create)
 }
@@ -369,6 +389,7 @@ __device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) 
 // use np.gradient's one-sided differences, REF/optical.py:160).  Returns false
 // (nothing written) when all four gradients are exactly zero and there are no
 // shadows: the caller then copies the quantised background.
+template <bool H16>
 __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env, int y, int xg,
                                             const float c[6], const float4 mm, const float4 nn,
                                             uint8_t* out) {
@@ -422,6 +443,28 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
     // two 256-bit loads per pixel: floats 0..7 and 8..15 of the bin
     const int i0 = planar_bin(p, a0p.mb, a0p.db);
     const int i1 = planar_bin(p, a1p.mb, a1p.db);
+    if constexpr (H16) {
+      // fp16 LUT: one 32-B sector per bin (half the gather bytes)
+      uint32_t w0[8], w1[8];
+      ld256u(p.lut_h16 + 2 * i0, w0);
+      ld256u(p.lut_h16 + 2 * i1, w1);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const Px& pp = s ? a1p : a0p;
+        float r = bgv[6 * h + 3 * s], g = bgv[6 * h + 3 * s + 1], b = bgv[6 * h + 3 * s + 2];
+        add_lut_h(s ? w1 : w0, pp.nx, pp.ny, r, g, b);
+        if (p.shadow) {
+          const float f = sf[2 * h + s];
+          r = clampf(r, 0.f, 255.f) * f;
+          g = clampf(g, 0.f, 255.f) * f;
+          b = clampf(b, 0.f, 255.f) * f;
+        }
+        qb[6 * h + 3 * s] = u8sat(r);
+        qb[6 * h + 3 * s + 1] = u8sat(g);
+        qb[6 * h + 3 * s + 2] = u8sat(b);
+      }
+      continue;
+    }
     float4 a0, c0, d0, e0, a1, c1, d1, e1;
     {
       // plane 0 through the LSU (256-bit), plane 1 through the texture path:
@@ -464,6 +507,7 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
 #ifndef TAC_K2_MINB
 #define TAC_K2_MINB 4
 #endif
+template <bool H16>
 __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __grid_constant__ FrameParams p) {
   const int W = p.W, H = p.H;
   const long long env = blockIdx.y;
@@ -505,7 +549,7 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
     if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
     if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
     const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
-    done = shade_group(p, env, yc, xg, c, mm, nn, out);
+    done = shade_group<H16>(p, env, yc, xg, c, mm, nn, out);
   }
   if (act && !done) {  // flat group: the quantised background
     const uint32_t* s = reinterpret_cast<const uint32_t*>(p.bg_u8 + ((long long)yc * W + xg) * 3);
@@ -648,7 +692,10 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm) {
       CK(cudaGetLastError());
     }
     tm->mark(0);
-    band_shade_kernel<<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    if (p.lut_h16)
+      band_shade_kernel<true><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    else
+      band_shade_kernel<false><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
     CK(cudaGetLastError());
     tm->mark(1);
   }

@@ -74,6 +74,7 @@ struct FrameParams {
   const float* lut_half;     // [2][nbins][8]: plane h holds floats 8h..8h+7 of every bin
   unsigned long long lut_tex;  // cudaTextureObject_t over lut_half as float4 texels (0 = none)
   const float* bg_planar;    // [3][H][W]
+  const uint4* lut_h16;      // lut_dtype f16: [nbins][2] uint4 = 16 fp16 (15 used), direction-major; else null
   int nbins;
   // io
   const float* in;

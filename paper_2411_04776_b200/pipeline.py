@@ -177,7 +177,8 @@ class TactilePipeline:
         if path == _lib.TAC_PATH_FUSED:
             return ["frame_kernel (fused)"]
         blur = "stream_blur_kernel" if path == _lib.TAC_PATH_STREAM else "band_blur_kernel"
-        return [blur, "band_shade_kernel", "env_epilogue_kernel"]
+        shade = "band_shade_kernel<f16 LUT>" if self.cfg.lut_dtype == "f16" else "band_shade_kernel"
+        return [blur, shade, "env_epilogue_kernel"]
 
     def launches_per_call(self, n_env):
         """Kernel launches one tac_pipeline call makes (diagnostics)."""
