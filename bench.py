@@ -253,11 +253,15 @@ def kernel_bytes(cfg, pipe):
     rr = cfg.dot_radius
     dot_px = sum(1 for dy in range(-rr, rr + 1) for dx in range(-rr, rr + 1) if dx * dx + dy * dy <= rr * rr)
     names = pipe.kernel_names()
-    if len(names) == 1:  # one fused frame kernel
-        return {names[0]: algorithmic_bytes(cfg)}
-    return dict(zip(names, (4 * h * w + 4 * h * w + 64 * bands,
-                            4 * h * w + 3 * h * w,
-                            64 * bands + 8 * r * c + 32 + 3 * dot_px * r * c)))
+    shadows = bool(cfg.shadows)
+    per = {"stream_blur_kernel": 4 * h * w + 4 * h * w + 64,
+           "band_blur_kernel": 4 * h * w + 4 * h * w + 64 * bands,
+           "band_shade_kernel": 4 * h * w + 3 * h * w + (4 * h * w if shadows else 0),
+           "env_epilogue_kernel": 64 * bands + 8 * r * c + 32 + 3 * dot_px * r * c,
+           "shadow_kernel": 4 * h * w + 4 * h * w,  # depth in, factor out
+           "frame_kernel (fused)": algorithmic_bytes(cfg)}
+    per["band_shade_kernel<f16 LUT>"] = per["band_shade_kernel"]
+    return {n: per[n] for n in names if n}
 
 
 # --------------------------------------------------------------------------- arms
@@ -478,8 +482,8 @@ def run_ours(a, rank, world, local_rank):
     step_gbs = per_launch / (k_ms / 1e3) / 1e9
     kb = kernel_bytes(cfg, pipe)
     kernels = {}
-    for name, kms in zip(kb, kern_ms):
-        if kms > 0:
+    for name, kms in zip(pipe.kernel_names(), kern_ms):
+        if name and kms > 0:
             gbs = kb[name] * n_env / (kms / 1e3) / 1e9
             kernels[name] = {"ms": kms, "bytes_per_frame": kb[name], "achieved_gbs": gbs, "frac": gbs / peak}
     dom = max(kernels, key=lambda k: kernels[k]["ms"])

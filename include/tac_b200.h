@@ -259,7 +259,8 @@ struct tac_pipeline_args {
   float* summary;           /* [N,8] out, nullable (tac_contact layout) */
   double* contact;          /* fp64 [N,8] out, nullable (tac_contact layout) */
   float* blurred;           /* [N,H,W] out, nullable (parity/debug) */
-  const float* shadow;      /* [N,H,W] shadow factor from tac_shadow, nullable (= no shadows) */
+  const float* shadow;      /* [N,H,W] shadow factor (e.g. from tac_shadow), nullable: with
+                               shadows on in the context the call runs the march itself */
   int32_t splat;            /* nonzero: draw marker dots into rgb */
   void* workspace;
   int64_t n_env;

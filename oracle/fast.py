@@ -12,7 +12,7 @@ reference.  ``tests/test_oracle_fast.py`` checks it against the oracle.
 import numpy as np
 from scipy import ndimage
 
-from . import marker
+from . import marker, optical
 
 
 class FastOracle:
@@ -35,6 +35,10 @@ class FastOracle:
         self.sten = (dy[m], dx[m])
         self.color = np.asarray(cfg.dot_color, dtype=np.uint8)
         self.threshold = cfg.contact_threshold
+        self.shadows = bool(getattr(cfg, "shadows", False))
+        if self.shadows:
+            self.light_dirs = np.asarray(cfg.light_dirs, dtype=np.float64)
+            self.shadow_args = (cfg.shadow_factor, cfg.shadow_steps, cfg.shadow_softness)
 
     def run(self, depth, shear, twist):
         ind = np.clip(self.rest - depth, 0.0, self.rest)
@@ -55,7 +59,12 @@ class FastOracle:
         coef = self.lut[mb * self.n_dir + db]  # (H, W, 3, 5)
         basis = np.stack([nx, ny, nx * nx, nx * ny, ny * ny], axis=-1)
         delta = np.einsum("hwck,hwk->hwc", coef, basis)
-        rgb = np.clip(np.rint(self.bg + delta), 0, 255).astype(np.uint8)
+        val = self.bg + delta
+        if self.shadows:  # add_shadows (REF/optical.py:261-300) on the clipped shading
+            f, steps, soft = self.shadow_args
+            sh = optical.shadow_factor(-depth, self.pitch, self.light_dirs, f, steps, soft)
+            val = np.clip(val, 0.0, 255.0) * sh[..., None]
+        rgb = np.clip(np.rint(val), 0, 255).astype(np.uint8)
         c = marker.contact_center(ind, self.pitch, self.threshold)
         load = dict(c)
         if c["in_contact"]:

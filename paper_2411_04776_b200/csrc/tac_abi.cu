@@ -121,6 +121,14 @@ size_t v5_workspace_bytes(const tac_ctx* c, int64_t n_env) {
          align256((size_t)C * p.bands * p.ext_strips * sizeof(int2)) + align256((size_t)C * p.H * p.W * sizeof(float));
 }
 
+// add_shadows factor computed by tac_pipeline itself (shadows on, no caller
+// factor): one chunk on the two-kernel path, every env on the fused path.
+size_t shadow_workspace_bytes(const tac_ctx* c, int64_t n_env) {
+  if (c->shadow.n_lights == 0) return 0;
+  const long long C = c->use5 ? std::min<long long>(n_env, c->chunk5) : n_env;
+  return align256((size_t)C * c->cfg.height * c->cfg.width * sizeof(float));
+}
+
 size_t v3_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   const size_t part = align256((size_t)n_env * c->max_tiles * kSumFields * sizeof(double));
   return part + align256((size_t)n_env * sizeof(unsigned int));
@@ -522,7 +530,7 @@ int tac_ctx_destroy(tac_ctx* ctx) { return free_ctx(ctx); }
 
 size_t tac_workspace_bytes(const tac_ctx* c, int64_t n_env) {
   if (!c || n_env < 0) return 0;
-  return v3_workspace_bytes(c, n_env) + v5_workspace_bytes(c, n_env);
+  return v3_workspace_bytes(c, n_env) + v5_workspace_bytes(c, n_env) + shadow_workspace_bytes(c, n_env);
 }
 
 int32_t tac_tiles_per_frame(const tac_ctx* c) { return c ? c->fused.strips : 0; }
@@ -707,13 +715,25 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
     tm.s = (cudaStream_t)stream;
   }
   cudaError_t e;
+  // the add_shadows march runs here when the context has shadows on and the
+  // caller gave no factor (REF/envs.py:1173 runs it on every observation)
+  float* shadow_ws = nullptr;
+  if (c->shadow.n_lights > 0 && a->shadow == nullptr)
+    shadow_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(a->workspace) + v3_workspace_bytes(c, a->n_env) +
+                                         v5_workspace_bytes(c, a->n_env));
   if (v5) {
     bind_workspace5(c, p, a->workspace, a->n_env);
-    e = launch_frame5(p, (cudaStream_t)stream, &tm);
+    e = launch_frame5(p, (cudaStream_t)stream, &tm, shadow_ws ? &c->shadow : nullptr, shadow_ws);
   } else {
     e = bind_workspace(c, p, a->workspace, a->n_env, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "tac_pipeline");
     tm.start();
+    if (shadow_ws) {
+      e = launch_shadow(c->shadow, a->in, p.input_depth, shadow_ws, nullptr, a->n_env, (cudaStream_t)stream);
+      if (e != cudaSuccess) return cuda_fail(e, "tac_pipeline (shadows)");
+      tm.mark(3);
+      p.shadow = shadow_ws;
+    }
     e = launch_frame(p, kModeFused, (cudaStream_t)stream);
     tm.mark(0);
   }

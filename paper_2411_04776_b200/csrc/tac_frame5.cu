@@ -653,7 +653,8 @@ int frame5_launches(const FrameParams& p, long long n_env) {
   return (int)(2 * ((n_env + chunk - 1) / chunk) + (p.finalize != 0 ? 1 : 0));
 }
 
-cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm) {
+cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm, const ShadowParams* sp,
+                          float* shadow_ws) {
   const size_t smem = band_blur_smem_bytes(p0);
   cudaError_t e = cudaFuncSetAttribute(band_blur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -685,6 +686,11 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm) {
     p.partials = p0.partials + e0 * p0.nparts * kSumFields;
     if (p0.shadow) p.shadow = p0.shadow + e0 * HW;
     p.n_env = n;
+    if (sp != nullptr) {  // add_shadows factor of this chunk (kind 3)
+      CK(launch_shadow(*sp, p.in, p.input_depth, shadow_ws, nullptr, n, s));
+      tm->mark(3);
+      p.shadow = shadow_ws;
+    }
     if (p.st_kind >= 0) {
       CK(launch_stream_blur(p, s));
     } else {

@@ -162,7 +162,10 @@ cudaError_t launch_frame(const FrameParams& p, int mode, cudaStream_t s);
 // band-tiled two-kernel path (tac_frame5.cu): one strip, W % 16 == 0, R <= 16
 bool frame5_eligible(const FrameParams& p);
 bool shade5_eligible(const FrameParams& p);
-cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, Marks* tm = nullptr);
+// sp / shadow_ws (nullable): run the add_shadows march per env chunk into
+// shadow_ws (chunk x H x W) before the chunk's blur and shade with it.
+cudaError_t launch_frame5(const FrameParams& p, cudaStream_t s, Marks* tm = nullptr, const ShadowParams* sp = nullptr,
+                          float* shadow_ws = nullptr);
 // row-streaming path (tac_stream.cu): plan (sets st_* / -1 when not
 // eligible), smem bytes, and the blur launch of one env chunk.
 void plan_stream(FrameParams& p);

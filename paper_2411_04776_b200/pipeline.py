@@ -1,8 +1,9 @@
 """The batched hot path: depth maps -> RGB tactile images + marker fields.
 
-``TactilePipeline.simulate`` is one ``tac_pipeline`` launch for all envs: the
+``TactilePipeline.simulate`` is one ``tac_pipeline`` call for all envs: the
 batched equivalent of the per-sensor loop of ``Environment._observe``
-(REF/envs.py:1156-1209) with shadows off, followed by the marker-dot splat of
+(REF/envs.py:1156-1209) -- including the ``add_shadows`` march when the
+config turns shadows on -- followed by the marker-dot splat of
 ``render_markers`` (REF/marker.py:203-234).
 """
 
@@ -40,7 +41,6 @@ class TactilePipeline:
         self.device = self.ctx.device
         self.H, self.W = self.ctx.H, self.ctx.W
         self.rows, self.cols = self.ctx.rows, self.ctx.cols
-        self._shadow = {}
 
     # -- buffers ---------------------------------------------------------------
     def allocate(self, n_env, *, blurred=False, contact=False):
@@ -52,15 +52,6 @@ class TactilePipeline:
             contact=torch.empty((n_env, 8), dtype=torch.float64, device=d) if contact else None,
             blurred=torch.empty((n_env, self.H, self.W), dtype=torch.float32, device=d) if blurred else None,
         )
-
-    def shadow_buffer(self, n_env):
-        """Per-stream scratch for the [N, H, W] shadow factor."""
-        key = (torch.cuda.current_stream(self.device).cuda_stream, n_env)
-        buf = self._shadow.get(key)
-        if buf is None:
-            buf = torch.empty((n_env, self.H, self.W), dtype=torch.float32, device=self.device)
-            self._shadow[key] = buf
-        return buf
 
     def new_state(self, n_env):
         """Zero LoadState per env (REF/marker.py:68-70), fp64 [N, 8]."""
@@ -129,13 +120,6 @@ class TactilePipeline:
         a.summary = out.summary.data_ptr() if out.summary is not None else None
         a.contact = out.contact.data_ptr() if out.contact is not None else None
         a.blurred = out.blurred.data_ptr() if out.blurred is not None else None
-        if self.cfg.shadows:
-            # add_shadows (REF/optical.py:261-300): march kernel, then the fused
-            # kernel multiplies the clipped shading by the factor before rounding
-            f = self.shadow_buffer(n)
-            _lib.check(self.ctx.lib.tac_shadow(self.ctx.handle, depth.data_ptr(), a.input_kind, f.data_ptr(),
-                                               None, n, self.ctx.stream()), "tac_shadow")
-            a.shadow = f.data_ptr()
         a.splat = 1 if splat else 0
         a.workspace = self.ctx.workspace(n).data_ptr()
         a.n_env = n
@@ -175,10 +159,11 @@ class TactilePipeline:
         """Kernel of each timing slot [blur, shade, epilogue] of this path."""
         path = self.path()
         if path == _lib.TAC_PATH_FUSED:
-            return ["frame_kernel (fused)"]
+            return ["frame_kernel (fused)"] + (["", "", "shadow_kernel"] if self.cfg.shadows else [])
         blur = "stream_blur_kernel" if path == _lib.TAC_PATH_STREAM else "band_blur_kernel"
         shade = "band_shade_kernel<f16 LUT>" if self.cfg.lut_dtype == "f16" else "band_shade_kernel"
-        return [blur, shade, "env_epilogue_kernel"]
+        names = [blur, shade, "env_epilogue_kernel"]
+        return names + ["shadow_kernel"] if self.cfg.shadows else names
 
     def launches_per_call(self, n_env):
         """Kernel launches one tac_pipeline call makes (diagnostics)."""
