@@ -1,6 +1,7 @@
 // C ABI: context lifetime, argument validation (error classes of
 // REF/errors.py), and kernel launches.  No CPU fallback: every compute entry
 // point enqueues CUDA work on the caller's stream or returns an error.
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -388,6 +389,30 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
     }
     sp.off = c->d_shadow_off;
     sp.cost = c->d_shadow_cost;
+    // tiled-march geometry: per light, the region of a kShadowTH x kShadowTW
+    // output tile shifted by every offset of that light
+    size_t region = 0;
+    for (int l = 0; l < lights; ++l) {
+      int dimn = INT_MAX, dimx = INT_MIN, djmn = INT_MAX, djmx = INT_MIN;
+      for (int st = 0; st < sp.steps; ++st) {
+        const int2 o = off[l * sp.steps + st];
+        dimn = std::min(dimn, o.x);
+        dimx = std::max(dimx, o.x);
+        djmn = std::min(djmn, o.y);
+        djmx = std::max(djmx, o.y);
+      }
+      sp.l_di_min[l] = dimn;
+      sp.l_dj_min[l] = djmn;
+      sp.l_rh[l] = kShadowTH + dimx - dimn;
+      sp.l_rw[l] = kShadowTW + djmx - djmn;
+      region = std::max(region, (size_t)sp.l_rh[l] * sp.l_rw[l] * sizeof(float));
+      for (int st = 0; st < sp.steps; ++st) {
+        const int2 o = off[l * sp.steps + st];
+        sp.offb[l][st] = ((o.x - dimn) * sp.l_rw[l] + (o.y - djmn)) * (int)sizeof(float);
+        sp.costs[l][st] = cost[l * sp.steps + st];
+      }
+    }
+    sp.tiled = lights > 0 && region <= 200 * 1024;
   }
 
   MarkerGeom& mg = c->mg;

@@ -140,14 +140,21 @@ struct Marks {
 };
 
 // add_shadows march tables (REF/optical.py:283-299), built on the host.
+constexpr int kShadowTH = 24, kShadowTW = 160;  // tiled march: output tile of one CTA
 struct ShadowParams {
   int H, W;
   int n_lights, steps;
-  const int2* off;       // [n_lights * steps] (di, dj)
+  const int2* off;       // [n_lights * steps] (di, dj)      (L1 fallback kernel)
   const float* cost;     // [n_lights * steps] s * pitch * lz / lateral
   float one_minus_factor;
   float inv_softness;
-  int di_min, di_max, dj_min, dj_max;  // offset bounds (interior fast path)
+  int di_min, di_max, dj_min, dj_max;  // offset bounds over all lights (interior fast path)
+  // tiled march: per light the tile's offset-range region [rh x rw] in smem
+  int tiled;                            // 1: smem-tiled kernel (region fits)
+  int l_di_min[TAC_MAX_LIGHTS], l_dj_min[TAC_MAX_LIGHTS];
+  int l_rh[TAC_MAX_LIGHTS], l_rw[TAC_MAX_LIGHTS];
+  int offb[TAC_MAX_LIGHTS][TAC_MAX_SHADOW_STEPS];    // byte offset of step s inside the light's region
+  float costs[TAC_MAX_LIGHTS][TAC_MAX_SHADOW_STEPS]; // s * rise (fp32)
 };
 
 cudaError_t launch_shadow(const ShadowParams& s, const float* in, int input_depth, float* factor,
