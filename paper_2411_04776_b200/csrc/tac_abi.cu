@@ -401,18 +401,21 @@ int tac_ctx_create(const tac_config* cfg, tac_ctx** out) {
         djmn = std::min(djmn, o.y);
         djmx = std::max(djmx, o.y);
       }
+      // region columns start at a multiple of 4 (tile origins are) so rows
+      // stage with 16-B loads; width a multiple of 4
+      const int dja = (int)std::floor(djmn / 4.0) * 4;
       sp.l_di_min[l] = dimn;
-      sp.l_dj_min[l] = djmn;
+      sp.l_dj_min[l] = dja;
       sp.l_rh[l] = kShadowTH + dimx - dimn;
-      sp.l_rw[l] = kShadowTW + djmx - djmn;
+      sp.l_rw[l] = (kShadowTW + djmx - dja + 3) & ~3;
       region = std::max(region, (size_t)sp.l_rh[l] * sp.l_rw[l] * sizeof(float));
       for (int st = 0; st < sp.steps; ++st) {
         const int2 o = off[l * sp.steps + st];
-        sp.offb[l][st] = ((o.x - dimn) * sp.l_rw[l] + (o.y - djmn)) * (int)sizeof(float);
+        sp.offb[l][st] = ((o.x - dimn) * sp.l_rw[l] + (o.y - dja)) * (int)sizeof(float);
         sp.costs[l][st] = cost[l * sp.steps + st];
       }
     }
-    sp.tiled = lights > 0 && region <= 200 * 1024;
+    sp.tiled = lights > 0 && region <= 72 * 1024 && k.width % 4 == 0;
   }
 
   MarkerGeom& mg = c->mg;

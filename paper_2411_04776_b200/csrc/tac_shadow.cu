@@ -97,17 +97,17 @@ __global__ void __launch_bounds__(kShadowTX * kShadowTY) shadow_kernel(
 
 constexpr int kTileThreads = 256;  // 8 warps x 3 rows; lanes x 5 columns
 
-// Paired fp32 subtraction (FADD2 on sm_100a).
-__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+// Paired fp32 addition (FADD2 on sm_100a).
+__device__ __forceinline__ float2 fadd2s(float2 a, float2 b) {
   float2 r;
   asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-      " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
       : "=f"(r.x), "=f"(r.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
 }
 
-__global__ void __launch_bounds__(kTileThreads, 2) shadow_tiled_kernel(
+__global__ void __launch_bounds__(kTileThreads, 3) shadow_tiled_kernel(
     const __grid_constant__ ShadowParams s, const float* __restrict__ in, int input_depth,
     float* __restrict__ factor, float* __restrict__ rgb, long long n_env) {
   extern __shared__ __align__(16) float reg[];
@@ -124,34 +124,46 @@ __global__ void __launch_bounds__(kTileThreads, 2) shadow_tiled_kernel(
   const long long HW = (long long)s.H * s.W;
   const float* e = in + env * HW;
   // elevation: -depth for a HeightMap; the indentation differs from it by a
-  // constant where the depth is within [0, rest], which cancels in occ
+  // constant where the depth is within [0, rest], which cancels in occ.  The
+  // region holds the raw input; the sign is applied to the max below.
   const float sg = input_depth ? -1.f : 1.f;
-  float e0[RPW][CPL], F[RPW][CPL];
+  float F[RPW][CPL];
 #pragma unroll
   for (int r = 0; r < RPW; ++r)
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int i = min(ti0 + warp * RPW + r, s.H - 1), j = min(tj0 + lane + 32 * q, s.W - 1);
-      e0[r][q] = sg * __ldg(e + (long long)i * s.W + j);
-      F[r][q] = 1.f;
-    }
+    for (int q = 0; q < CPL; ++q) F[r][q] = 1.f;
   for (int l = 0; l < s.n_lights; ++l) {
     const int rh = s.l_rh[l], rw = s.l_rw[l];
-    const int r0 = ti0 + s.l_di_min[l], c0 = tj0 + s.l_dj_min[l];
+    const int r0 = ti0 + s.l_di_min[l], c0 = tj0 + s.l_dj_min[l];  // c0, rw: multiples of 4
     if (l) __syncthreads();  // the previous light's region is no longer read
-    // stage the region (clamped indices = replicate border), rows by warp
+    // stage the region: rows by warp, 16-B groups by lane; row index clamped
+    // and groups outside [0, W) filled with the edge value (replicate border)
     for (int rr = warp; rr < rh; rr += 8) {
       const float* src = e + (long long)min(max(r0 + rr, 0), s.H - 1) * s.W;
-      float* dst = reg + rr * rw;
-      for (int cc = lane; cc < rw; cc += 32) dst[cc] = sg * __ldg(src + min(max(c0 + cc, 0), s.W - 1));
+      float4* dst = reinterpret_cast<float4*>(reg + rr * rw);
+      for (int g = lane; g < (rw >> 2); g += 32) {
+        const int cc = c0 + 4 * g;
+        float4 v;
+        if (cc < 0) {
+          const float x = __ldg(src);
+          v = make_float4(x, x, x, x);
+        } else if (cc >= s.W) {
+          const float x = __ldg(src + s.W - 1);
+          v = make_float4(x, x, x, x);
+        } else {
+          v = __ldg(reinterpret_cast<const float4*>(src + cc));
+        }
+        dst[g] = v;
+      }
     }
     __syncthreads();
+    // elev - c = sg (x - sg c): occ' = max_s (x - sg c) for sg = 1, min_s for
+    // sg = -1, and sg occ' = max_s (elev(p + o_s) - s rise), bit for bit
     float occ[RPW][CPL];
 #pragma unroll
     for (int r = 0; r < RPW; ++r)
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) occ[r][q] = -INFINITY;
-    // the pixel's own position inside the region (offsets carry -di_min, -dj_min)
+      for (int q = 0; q < CPL; ++q) occ[r][q] = INFINITY;
     const char* base = reinterpret_cast<const char*>(reg + (warp * RPW) * rw + lane);
     const int* offb = s.offb[l];
     const float* cost = s.costs[l];
@@ -159,33 +171,37 @@ __global__ void __launch_bounds__(kTileThreads, 2) shadow_tiled_kernel(
     for (; st + 1 < s.steps; st += 2) {
       const char* b0 = base + offb[st];
       const char* b1 = base + offb[st + 1];
-      const float2 cs = make_float2(cost[st], cost[st + 1]);
+      const float2 cs = make_float2(-sg * cost[st], -sg * cost[st + 1]);  // a = x - sg c
 #pragma unroll
       for (int r = 0; r < RPW; ++r)
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
           const int o = (r * rw + 32 * q) * (int)sizeof(float);
           // two steps of one pixel: one FADD2, one FMNMX3
-          const float2 a = fsub2(make_float2(*reinterpret_cast<const float*>(b0 + o),
-                                             *reinterpret_cast<const float*>(b1 + o)), cs);
-          occ[r][q] = fmaxf(occ[r][q], fmaxf(a.x, a.y));
+          const float2 a = fadd2s(make_float2(*reinterpret_cast<const float*>(b0 + o),
+                                              *reinterpret_cast<const float*>(b1 + o)), cs);
+          occ[r][q] = sg < 0.f ? fminf(occ[r][q], fminf(a.x, a.y)) : fmaxf(occ[r][q], fmaxf(a.x, a.y));
         }
     }
     if (st < s.steps) {
       const char* b0 = base + offb[st];
-      const float c0s = cost[st];
+      const float c0s = -sg * cost[st];
 #pragma unroll
       for (int r = 0; r < RPW; ++r)
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
-          occ[r][q] = fmaxf(occ[r][q], *reinterpret_cast<const float*>(b0 + (r * rw + 32 * q) * (int)sizeof(float)) - c0s);
+        for (int q = 0; q < CPL; ++q) {
+          const float a = *reinterpret_cast<const float*>(b0 + (r * rw + 32 * q) * (int)sizeof(float)) + c0s;
+          occ[r][q] = sg < 0.f ? fminf(occ[r][q], a) : fmaxf(occ[r][q], a);
+        }
     }
-    // occ = max_s (elev(p + o_s) - s * rise); weight = clip((occ - elev(p)) / softness, 0, 1)
+    // weight = clip((max_s(elev(p + o_s) - s rise) - elev(p)) / softness, 0, 1)
 #pragma unroll
     for (int r = 0; r < RPW; ++r)
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
-        const float w = fminf(fmaxf((occ[r][q] - e0[r][q]) * s.inv_softness, 0.f), 1.f);
+        const int i = min(ti0 + warp * RPW + r, s.H - 1), j = min(tj0 + lane + 32 * q, s.W - 1);
+        const float e0 = __ldg(e + (long long)i * s.W + j);
+        const float w = fminf(fmaxf(sg * (occ[r][q] - e0) * s.inv_softness, 0.f), 1.f);
         F[r][q] *= 1.f - s.one_minus_factor * w;
       }
   }
