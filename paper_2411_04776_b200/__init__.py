@@ -57,6 +57,7 @@ _LAZY = {
     "marker_displacements": ".marker",
     "render_markers": ".marker",
     "marker_config": ".marker",
+    "observation_digest": ".digest",
 }
 
 

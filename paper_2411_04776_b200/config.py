@@ -17,14 +17,24 @@ DEFAULT_PYRAMID = (5, 11, 21, 31)  # REF/tactile.py:22
 DEFAULT_CONTACT_THRESHOLD = 5e-5  # REF/marker.py:22
 
 
+_IDENTITY_POSE = tuple(float(v) for v in np.eye(4).ravel())
+
+
 @dataclass(frozen=True)
 class SensorConfig:
-    """Geometry of one tactile sensor (REF/tactile.py:31-69)."""
+    """Geometry of one tactile sensor (REF/tactile.py:31-69).
+
+    ``camera_pose_in_case``: the camera frame in the sensor case frame
+    (REF/tactile.py:47, used as ``case_pose.compose(camera_pose_in_case)`` at
+    REF/envs.py:733-734), here a 4x4 homogeneous rigid transform stored as
+    16 row-major floats (any 4x4 array-like is accepted); identity by default.
+    """
 
     image_size: Tuple[int, int] = (480, 640)
     sensing_area: Tuple[float, float] = (0.016, 0.012)
     gelpad_thickness: float = 0.004
     marker_grid: Tuple[int, int] = (10, 10)
+    camera_pose_in_case: Tuple[float, ...] = _IDENTITY_POSE
 
     def __post_init__(self):
         h, w = self.image_size
@@ -39,6 +49,18 @@ class SensorConfig:
             raise InvalidArgumentError("marker_grid must be positive")
         if abs(aw / w - ah / h) > 1e-12:
             raise InvalidArgumentError("sensing_area and image_size imply unequal x/y pixel pitch")
+        t = np.asarray(self.camera_pose_in_case, dtype=np.float64).reshape(-1)
+        if t.size != 16 or not np.isfinite(t).all():
+            raise InvalidArgumentError("camera_pose_in_case must be a finite 4x4 transform")
+        m = t.reshape(4, 4)
+        if not np.allclose(m[3], [0, 0, 0, 1]) or not np.allclose(m[:3, :3] @ m[:3, :3].T, np.eye(3), atol=1e-9):
+            raise InvalidArgumentError("camera_pose_in_case must be a rigid transform (orthonormal rotation)")
+        object.__setattr__(self, "camera_pose_in_case", tuple(float(v) for v in t))
+
+    @property
+    def camera_pose_matrix(self) -> np.ndarray:
+        """camera_pose_in_case as a 4x4 float64 array."""
+        return np.asarray(self.camera_pose_in_case, dtype=np.float64).reshape(4, 4)
 
     @property
     def pixel_pitch(self) -> float:

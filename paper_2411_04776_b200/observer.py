@@ -97,6 +97,13 @@ class SensorObserver:
             self.state[m] = 0.0
             self.prev_cam[m] = cam[m]
 
+    def camera_poses(self, case_poses):
+        """Camera-to-world poses of the sensors from their case poses [N, 4, 4]:
+        ``case_pose.compose(cfg.camera_pose_in_case)`` (REF/envs.py:733-734)."""
+        case = torch.as_tensor(case_poses, dtype=torch.float64, device=self.device)
+        t = torch.as_tensor(self.cfg.sensor.camera_pose_matrix, device=self.device)
+        return case @ t
+
     def _poses(self, cam):
         cam = torch.as_tensor(cam, dtype=torch.float64, device=self.device)
         if cam.shape != (self.n, 4, 4):

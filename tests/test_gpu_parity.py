@@ -624,6 +624,49 @@ class TestSensorObserver:
         obsr.reset(torch.as_tensor(cam), mask=torch.tensor([True, False, False]))
         assert not obsr.state[0].any() and obsr.state[1].any()
 
+    def test_replay_digests_identical_and_case_frame(self, golden):
+        """A replayed episode is bit-identical step by step (the reference's
+        c7 determinism check, REF/tests/test_acceptance.py:265-282, via
+        observation_digest), and observing from case poses composes
+        camera_pose_in_case (REF/envs.py:733-734)."""
+        from scipy.spatial.transform import Rotation
+
+        from paper_2411_04776_b200 import SensorObserver, observation_digest
+        from paper_2411_04776_b200.config import SensorConfig
+
+        g = golden("raster")
+        t_cam = np.eye(4)
+        t_cam[:3, 3] = (2e-5, -1e-5, 0.0)
+        base = small_config(48, 64)
+        sensor = SensorConfig(base.sensor.image_size, base.sensor.sensing_area, base.sensor.gelpad_thickness,
+                              base.sensor.marker_grid, camera_pose_in_case=t_cam)
+        cfg = dataclasses.replace(base, sensor=sensor)
+        n = 2
+        verts = torch.as_tensor(np.stack([g["verts_cam_1"], g["verts_cam_2"]]))
+        tris = torch.as_tensor(g["tris_0"])
+        rng = np.random.default_rng(11)
+        cases = [np.stack([np.eye(4)] * n)]
+        for _ in range(4):
+            step = np.eye(4)
+            step[:3, :3] = Rotation.from_rotvec([0, 0, rng.uniform(-0.02, 0.02)]).as_matrix()
+            step[:3, 3] = [rng.uniform(-3e-5, 3e-5), rng.uniform(-3e-5, 3e-5), 0.0]
+            cases.append(cases[-1] @ step)
+        obsr = SensorObserver(cfg, n, DEV, keep_heightmap=True)
+
+        def episode():
+            obsr.reset(obsr.camera_poses(cases[0]))
+            out = []
+            for t, case in enumerate(cases):
+                cam = obsr.camera_poses(case)
+                assert torch.allclose(cam.cpu(), torch.as_tensor(case @ t_cam))
+                o = obsr.observe(cam, verts_world=verts, tris=tris)
+                out.append(observation_digest(o, t, per_env=True))
+            return out
+
+        first, again = episode(), episode()
+        assert again == first
+        assert len({d for step in first for d in step}) == n * len(cases)
+
 
 class TestBandPathShapes:
     """The default two-kernel path (tac_frame5.cu) at shapes that exercise its
