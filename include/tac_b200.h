@@ -205,7 +205,8 @@ int tac_shade_ex(const tac_ctx* ctx, const float* blurred, uint8_t* rgb, uint32_
  *   exactly what the reference returns;
  * summary (nullable): fp32 [N,8] = {in_contact, area m^2, c_x m, c_y m,
  *   d_c m, force proxy m^3 (sum of indentation * p^2 over the contact mask),
- *   number of non-finite inputs, 0}. */
+ *   number of non-finite inputs, clipped channel values (tac_pipeline with
+ *   a `saturated` output, else 0)}. */
 int tac_contact(const tac_ctx* ctx, const float* in, int32_t input_kind,
                 double* contact, float* summary, void* workspace, int64_t n_env,
                 void* stream);
@@ -262,6 +263,9 @@ struct tac_pipeline_args {
   const float* shadow;      /* [N,H,W] shadow factor (e.g. from tac_shadow), nullable: with
                                shadows on in the context the call runs the march itself */
   int32_t splat;            /* nonzero: draw marker dots into rgb */
+  uint32_t* saturated;      /* [N] out, nullable: channel values the [0, 255] clip changed (the
+                               count behind REF/optical.py:246-249's >1 % warning); also
+                               written to summary field 7 */
   void* workspace;
   int64_t n_env;
 };

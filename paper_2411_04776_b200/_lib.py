@@ -101,6 +101,7 @@ class TacPipelineArgs(ctypes.Structure):
         ("blurred", _p),
         ("shadow", _p),
         ("splat", _i32),
+        ("saturated", _p),
         ("workspace", _p),
         ("n_env", _i64),
     ]

@@ -732,6 +732,13 @@ int tac_pipeline(const tac_ctx* c, const tac_pipeline_args* a, void* stream) {
   p.pose_delta = a->pose_delta;
   p.disp = a->disp;
   p.splat = a->splat;
+  p.saturated = a->saturated;
+  if (a->saturated && a->n_env > 0) {
+    if (!v5)
+      return fail(TAC_ERR_UNSUPPORTED, "the saturation count needs the two-kernel path (this frame uses the fused kernel)");
+    cudaError_t z = cudaMemsetAsync(a->saturated, 0, sizeof(uint32_t) * a->n_env, (cudaStream_t)stream);
+    if (z != cudaSuccess) return cuda_fail(z, "tac_pipeline");
+  }
   p.shadow = a->shadow;
   // diagnostics timeline (tac_timing_begin .. tac_timing_end)
   Marks tm;

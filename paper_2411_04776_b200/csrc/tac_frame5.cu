@@ -389,10 +389,16 @@ __device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) 
 // use np.gradient's one-sided differences, REF/optical.py:160).  Returns false
 // (nothing written) when all four gradients are exactly zero and there are no
 // shadows: the caller then copies the quantised background.
+// Channel values the [0, 255] clip changes (REF/optical.py:246-247:
+// raw != clip(raw), before any shadow), counted when the caller asks.
+__device__ __forceinline__ unsigned clip_count(float r, float g, float b) {
+  return (r < 0.f || r > 255.f ? 1u : 0u) + (g < 0.f || g > 255.f ? 1u : 0u) + (b < 0.f || b > 255.f ? 1u : 0u);
+}
+
 template <bool H16>
 __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env, int y, int xg,
                                             const float c[6], const float4 mm, const float4 nn,
-                                            uint8_t* out) {
+                                            uint8_t* out, unsigned& nsat) {
   const int W = p.W, H = p.H;
   const float m[4] = {mm.x, mm.y, mm.z, mm.w};
   const float n[4] = {nn.x, nn.y, nn.z, nn.w};
@@ -453,6 +459,7 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
         const Px& pp = s ? a1p : a0p;
         float r = bgv[6 * h + 3 * s], g = bgv[6 * h + 3 * s + 1], b = bgv[6 * h + 3 * s + 2];
         add_lut_h(s ? w1 : w0, pp.nx, pp.ny, r, g, b);
+        if (p.saturated) nsat += clip_count(r, g, b);
         if (p.shadow) {
           const float f = sf[2 * h + s];
           r = clampf(r, 0.f, 255.f) * f;
@@ -485,6 +492,7 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
         add_lut(a1, c1, d1, e1, pp.nx, pp.ny, r, g, b);
       else
         add_lut(a0, c0, d0, e0, pp.nx, pp.ny, r, g, b);
+      if (p.saturated) nsat += clip_count(r, g, b);
       if (p.shadow) {  // clip, then the multiplicative shadow (REF/optical.py:246, :299)
         const float f = sf[2 * h + s];
         r = clampf(r, 0.f, 255.f) * f;
@@ -545,11 +553,12 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
   float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
   bool done = false;
+  unsigned nsat = 0;
   if (any) {
     if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
     if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
     const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
-    done = shade_group<H16>(p, env, yc, xg, c, mm, nn, out);
+    done = shade_group<H16>(p, env, yc, xg, c, mm, nn, out, nsat);
   }
   if (act && !done) {  // flat group: the quantised background
     const uint32_t* s = reinterpret_cast<const uint32_t*>(p.bg_u8 + ((long long)yc * W + xg) * 3);
@@ -557,6 +566,10 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
     d[0] = __ldg(s);
     d[1] = __ldg(s + 1);
     d[2] = __ldg(s + 2);
+  }
+  if (p.saturated) {  // whole CTA is one env: one atomic per warp
+    const unsigned w = __reduce_add_sync(0xffffffffu, nsat);
+    if (lane == 0 && w) atomicAdd(p.saturated + env, w);
   }
 }
 

@@ -316,7 +316,7 @@ __device__ void finalize_load(const FrameParams& p, long long env, double cnt, d
     s[4] = (float)c.dmax;
     s[5] = c.in_contact ? (float)(sw * pitch * pitch) : 0.f;
     s[6] = (float)nf;
-    s[7] = 0.f;
+    s[7] = p.saturated != nullptr ? (float)p.saturated[env] : 0.f;
   }
   if (p.contact != nullptr) load_store(p.contact + env * 8, c);
   Load l = c;

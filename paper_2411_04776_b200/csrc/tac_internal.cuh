@@ -98,6 +98,7 @@ struct FrameParams {
   float* disp;           // nullable
   int splat;
   const float* shadow;   // nullable [N][H][W] multiplicative shadow factor
+  unsigned int* saturated;  // nullable [N]: clipped channel values per env (zeroed per call)
   // band-tiled two-kernel path (tac_frame5.cu)
   int bands;             // ceil(H / 16)
   long long chunk;       // envs per (blur, shade) launch pair

@@ -30,6 +30,7 @@ class Observation:
     summary: Optional[torch.Tensor]  # [N, 8] float32 (SUMMARY_FIELDS)
     contact: Optional[torch.Tensor] = None  # [N, 8] float64 LoadState of contact_center
     blurred: Optional[torch.Tensor] = None  # [N, H, W] float32 smoothed indentation
+    saturated: Optional[torch.Tensor] = None  # [N] int32 channel values the [0, 255] clip changed
 
 
 class TactilePipeline:
@@ -43,7 +44,7 @@ class TactilePipeline:
         self.rows, self.cols = self.ctx.rows, self.ctx.cols
 
     # -- buffers ---------------------------------------------------------------
-    def allocate(self, n_env, *, blurred=False, contact=False):
+    def allocate(self, n_env, *, blurred=False, contact=False, saturation=False):
         d = self.device
         return Observation(
             rgb=torch.empty((n_env, self.H, self.W, 3), dtype=torch.uint8, device=d),
@@ -51,6 +52,7 @@ class TactilePipeline:
             summary=torch.empty((n_env, 8), dtype=torch.float32, device=d),
             contact=torch.empty((n_env, 8), dtype=torch.float64, device=d) if contact else None,
             blurred=torch.empty((n_env, self.H, self.W), dtype=torch.float32, device=d) if blurred else None,
+            saturated=torch.empty((n_env,), dtype=torch.int32, device=d) if saturation else None,
         )
 
     def new_state(self, n_env):
@@ -71,6 +73,7 @@ class TactilePipeline:
         blurred=False,
         contact=False,
         splat=True,
+        saturation=False,
     ) -> Observation:
         """Run the whole path for every env in one ``tac_pipeline`` call
         (band blur + band shade kernels and a per-env epilogue).
@@ -81,6 +84,9 @@ class TactilePipeline:
         (rad) given directly (BASELINE configs[2]), or ``state`` [N, 8] fp64
         LoadState advanced in place by ``pose_delta`` [N, 3] = (dx, dy,
         rotvec_z) through ``track_load`` (REF/marker.py:124-140).
+        ``saturation=True`` also counts, per env, the channel values the
+        [0, 255] clip changed (``out.saturated`` and summary field 7: the
+        count behind the reference's >1 % warning, REF/optical.py:246-249).
         """
         d = self.device
         n = int(depth.shape[0]) if isinstance(depth, torch.Tensor) and depth.dim() == 3 else -1
@@ -88,7 +94,7 @@ class TactilePipeline:
         if input_kind not in ("depth", "indentation"):
             raise InvalidArgumentError("input_kind must be 'depth' or 'indentation'")
         if out is None:
-            out = self.allocate(n, blurred=blurred, contact=contact)
+            out = self.allocate(n, blurred=blurred, contact=contact, saturation=saturation)
         require(out.rgb, "rgb", torch.uint8, (n, self.H, self.W, 3), d)
         if out.disp is not None:
             require(out.disp, "disp", torch.float32, (n, self.rows, self.cols, 2), d)
@@ -98,6 +104,8 @@ class TactilePipeline:
             require(out.contact, "contact", torch.float64, (n, 8), d)
         if out.blurred is not None:
             require(out.blurred, "blurred", torch.float32, (n, self.H, self.W), d)
+        if out.saturated is not None:
+            require(out.saturated, "saturated", torch.int32, (n,), d)
         a = _lib.TacPipelineArgs()
         a.in_ = depth.data_ptr()
         a.input_kind = _lib.TAC_INPUT_DEPTH if input_kind == "depth" else _lib.TAC_INPUT_INDENTATION
@@ -120,6 +128,7 @@ class TactilePipeline:
         a.summary = out.summary.data_ptr() if out.summary is not None else None
         a.contact = out.contact.data_ptr() if out.contact is not None else None
         a.blurred = out.blurred.data_ptr() if out.blurred is not None else None
+        a.saturated = out.saturated.data_ptr() if out.saturated is not None else None
         a.splat = 1 if splat else 0
         a.workspace = self.ctx.workspace(n).data_ptr()
         a.n_env = n

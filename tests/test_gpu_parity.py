@@ -902,3 +902,25 @@ class TestParityAtScale:
             assert normwise(obs.blurred[i].cpu().numpy(), ref["blurred"]) <= BLUR_TOL
             assert normwise(obs.disp[i].cpu().numpy(), ref["disp"]) <= DISP_TOL
         assert worst >= RGB_FRAC
+
+
+def test_pipeline_saturation_count_matches_standalone_shade():
+    """tac_pipeline's per-env clip count (summary field 7) equals the
+    standalone shade's count on the same smoothed map (REF/optical.py:246-249)."""
+    base = small_config(48, 64)
+    cfg = dataclasses.replace(base, lut=base.lut * 60.0)  # steep LUT: many clipped channels
+    depth = depth_batch(4, 48, 64, seed=97)
+    shear, twist = synthetic.loads(4, 98)
+    obs = run_pipeline(cfg, depth, shear, twist, splat=False, saturation=True)
+    from paper_2411_04776_b200.context import context_for
+    from paper_2411_04776_b200 import _lib
+
+    ctx = context_for(cfg, DEV)
+    out = torch.empty((4, 48, 64, 3), dtype=torch.uint8, device=DEV)
+    sat = torch.empty((4,), dtype=torch.int32, device=DEV)
+    _lib.check(ctx.lib.tac_shade_ex(ctx.handle, obs.blurred.data_ptr(), out.data_ptr(), sat.data_ptr(), 4,
+                                    ctx.stream()), "tac_shade_ex")
+    torch.cuda.synchronize()
+    assert torch.equal(obs.saturated.cpu(), sat.cpu())
+    assert int(sat.sum()) > 0
+    assert torch.equal(obs.summary[:, 7].cpu(), sat.float().cpu())
