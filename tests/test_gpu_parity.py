@@ -908,7 +908,8 @@ def test_pipeline_saturation_count_matches_standalone_shade():
     """tac_pipeline's per-env clip count (summary field 7) equals the
     standalone shade's count on the same smoothed map (REF/optical.py:246-249)."""
     base = small_config(48, 64)
-    cfg = dataclasses.replace(base, lut=base.lut * 60.0)  # steep LUT: many clipped channels
+    # steep LUT over a near-white background: many clipped channels
+    cfg = dataclasses.replace(base, lut=base.lut * 60.0, background=np.full_like(base.background, 254.0))
     depth = depth_batch(4, 48, 64, seed=97)
     shear, twist = synthetic.loads(4, 98)
     obs = run_pipeline(cfg, depth, shear, twist, splat=False, saturation=True)
