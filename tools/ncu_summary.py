@@ -50,7 +50,12 @@ lines, traffic = [], {}
 for vals in rows[2:]:
     d = {n: (vals[i], units[i]) for i, n in enumerate(h)}
     name = d["Kernel Name"][0]
-    short = re.sub(r"\(.*", "", name).split("::")[-1].split(" ")[-1]
+    m = re.search(r"(\w+_kernel)(<(\w+)>)?", name)
+    short = m.group(1) if m else name
+    if short == "band_shade_kernel" and m.group(3) in ("true", "1"):
+        short = "band_shade_kernel<f16 LUT>"
+    if short == "shadow_tiled_kernel":
+        short = "shadow_kernel"  # bench.py's name for the march
     lines += [f"## {name}", "", "| metric | value |", "|---|---|"]
     for k, label in want:
         if k in d:
@@ -79,5 +84,5 @@ if key:
     entry = dict(traffic)
     if envs:
         entry["envs"] = envs
-    doc[key] = entry
+    doc.setdefault(key, {}).update(entry)
     json.dump(doc, open(tpath, "w"), indent=1)
