@@ -55,6 +55,10 @@ constexpr int BH = 16;    // band rows
 constexpr int K1T = 320;  // blur threads: 8 row pairs x 40 chunks of 8 columns (W = 320)
 constexpr int K2T = 320;     // shade threads per CTA, at most
 constexpr int K2_MIN = 160;  // preferred smallest shade CTA (measured: 160 > 320 > 640 threads at W = 320)
+#ifndef TAC_SHADE_ROW_ITERS
+#define TAC_SHADE_ROW_ITERS 8
+#endif
+constexpr int kShadeRowIters = TAC_SHADE_ROW_ITERS;  // row iterations per shade thread
 
 // ---- row-pair interleaved intermediate ----------------------------------------
 // vb2[m][col] = (V[2m][col], V[2m+1][col]) as float2: the horizontal FFMA2
@@ -521,51 +525,56 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   const long long env = blockIdx.y;
   const int gi = threadIdx.x;
   const int ng = blockDim.x;  // 4-pixel groups per row
-  const int y = blockIdx.x * blockDim.y + threadIdx.y;
   const int xg = 4 * gi;
   const long long HW = (long long)H * W;
   const int lane = (threadIdx.y * ng + gi) & 31;
-  const bool act = y < H;
-  const int yc = act ? y : H - 1;
-  const float* rc = p.scratch + env * HW + (long long)yc * W + xg;
+  const float* img = p.scratch + env * HW + xg;
   uint8_t* out = p.rgb + env * HW * 3;
-
-  // columns whose gradient can be non-zero: band extents of rows y-1..y+1
-  // (union over the blur kernel's column strips), +-1
   const int ns = p.ext_strips;
   const int2* ext = p.band_ext + env * p.bands * ns;
-  const int ba = max(yc - 1, 0) >> 4, bb = min(yc + 1, H - 1) >> 4;
-  int sa = INT_MAX, sb = INT_MIN;
-  for (int s = 0; s < ns; ++s) {
-    const int2 e0 = __ldg(ext + ba * ns + s);
-    const int2 e1 = __ldg(ext + bb * ns + s);
-    sa = min(sa, min(e0.x, e1.x));
-    sb = max(sb, max(e0.y, e1.y));
-  }
-  // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
-  const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
-  float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
-  if (any) {
-    cc = *reinterpret_cast<const float4*>(rc);
-    mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
-    nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
-  }
-  float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
-  float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
-  bool done = false;
   unsigned nsat = 0;
-  if (any) {
-    if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
-    if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
-    const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
-    done = shade_group<H16>(p, env, yc, xg, c, mm, nn, out, nsat);
-  }
-  if (act && !done) {  // flat group: the quantised background
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(p.bg_u8 + ((long long)yc * W + xg) * 3);
-    uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)yc * W + xg) * 3);
-    d[0] = __ldg(s);
-    d[1] = __ldg(s + 1);
-    d[2] = __ldg(s + 2);
+  // each CTA shades kShadeRowIters x blockDim.y rows of one env (setup amortised)
+#pragma unroll 1
+  for (int it = 0; it < kShadeRowIters; ++it) {
+    const int y = (blockIdx.x * kShadeRowIters + it) * blockDim.y + threadIdx.y;
+    if (__all_sync(0xffffffffu, y >= H)) break;  // warps hold whole rows: uniform per warp
+    const bool act = y < H;
+    const int yc = act ? y : H - 1;
+    const float* rc = img + (long long)yc * W;
+    // columns whose gradient can be non-zero: band extents of rows y-1..y+1
+    // (union over the blur kernel's column strips), +-1
+    const int ba = max(yc - 1, 0) >> 4, bb = min(yc + 1, H - 1) >> 4;
+    int sa = INT_MAX, sb = INT_MIN;
+    for (int s = 0; s < ns; ++s) {
+      const int2 e0 = __ldg(ext + ba * ns + s);
+      const int2 e1 = __ldg(ext + bb * ns + s);
+      sa = min(sa, min(e0.x, e1.x));
+      sb = max(sb, max(e0.y, e1.y));
+    }
+    // (with shadows every pixel is shaded: the shadow factor reaches flat regions)
+    const bool any = act && ((sa <= sb && xg <= sb + 1 && xg + 3 >= sa - 1) || p.shadow != nullptr);
+    float4 cc = make_float4(0.f, 0.f, 0.f, 0.f), mm = cc, nn = cc;
+    if (any) {
+      cc = *reinterpret_cast<const float4*>(rc);
+      mm = *reinterpret_cast<const float4*>(yc > 0 ? rc - W : rc);
+      nn = *reinterpret_cast<const float4*>(yc < H - 1 ? rc + W : rc);
+    }
+    float left = __shfl_up_sync(0xffffffffu, cc.w, 1);
+    float right = __shfl_down_sync(0xffffffffu, cc.x, 1);
+    bool done = false;
+    if (any) {
+      if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
+      if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
+      const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
+      done = shade_group<H16>(p, env, yc, xg, c, mm, nn, out, nsat);
+    }
+    if (act && !done) {  // flat group: the quantised background
+      const uint32_t* s = reinterpret_cast<const uint32_t*>(p.bg_u8 + ((long long)yc * W + xg) * 3);
+      uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)yc * W + xg) * 3);
+      d[0] = __ldg(s);
+      d[1] = __ldg(s + 1);
+      d[2] = __ldg(s + 2);
+    }
   }
   if (p.saturated) {  // whole CTA is one env: one atomic per warp
     const unsigned w = __reduce_add_sync(0xffffffffu, nsat);
@@ -677,7 +686,7 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm, cons
   const dim3 b1(ng, K1T / ng);
   const int rpc = shade_rows_per_cta(ng);
   const dim3 b2(ng, rpc);
-  const unsigned nq = (unsigned)((p0.H + rpc - 1) / rpc);
+  const unsigned nq = (unsigned)((p0.H + rpc * kShadeRowIters - 1) / (rpc * kShadeRowIters));
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
   const long long nchunks = (p0.n_env + chunk - 1) / chunk;
   Marks none;
