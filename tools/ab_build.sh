@@ -8,7 +8,7 @@ out=/tmp/ab_$1; mkdir -p $out
 NV="nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -ftz=true -Xcompiler -fPIC --expt-relaxed-constexpr"
 objs=""
 for f in $(sed -n 's/^SRCS := //p' Makefile | sed 's/\.cu//g'); do
-  if [ "$f" = "tac_frame5" ]; then $NV $2 -c $f.cu -o $out/$f.o; objs="$objs $out/$f.o"; else objs="$objs build/$f.o"; fi
+  if [ "$f" = "tac_frame5" ] || [ "$f" = "tac_stream" ]; then $NV $2 -c $f.cu -o $out/$f.o; objs="$objs $out/$f.o"; else objs="$objs build/$f.o"; fi
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libtac_b200_$1.so $objs
 echo built ../libtac_b200_$1.so
