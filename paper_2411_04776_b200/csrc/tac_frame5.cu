@@ -59,6 +59,10 @@ constexpr int K2_MIN = 160;  // preferred smallest shade CTA (measured: 160 > 32
 #define TAC_SHADE_ROW_ITERS 8
 #endif
 constexpr int kShadeRowIters = TAC_SHADE_ROW_ITERS;  // row iterations per shade thread
+#ifndef TAC_SHADE_UNROLL
+#define TAC_SHADE_UNROLL 1
+#endif
+constexpr int kShadeUnroll = TAC_SHADE_UNROLL;
 
 // ---- row-pair interleaved intermediate ----------------------------------------
 // vb2[m][col] = (V[2m][col], V[2m+1][col]) as float2: the horizontal FFMA2
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
   const int2* ext = p.band_ext + env * p.bands * ns;
   unsigned nsat = 0;
   // each CTA shades kShadeRowIters x blockDim.y rows of one env (setup amortised)
-#pragma unroll 1
+#pragma unroll kShadeUnroll
   for (int it = 0; it < kShadeRowIters; ++it) {
     const int y = (blockIdx.x * kShadeRowIters + it) * blockDim.y + threadIdx.y;
     if (__all_sync(0xffffffffu, y >= H)) break;  // warps hold whole rows: uniform per warp
