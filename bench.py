@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--shadows", action="store_true", help="add_shadows on (REF/optical.py:261-300)")
     ap.add_argument("--lut-dtype", default="f32", choices=["f32", "f16"])
     ap.add_argument("--kernel-path", default="auto", choices=["auto", "stream", "band", "fused"])
+    ap.add_argument("--chunk-envs", type=int, default=0, help="envs per blur/shade launch pair (0 = library default)")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -62,7 +63,7 @@ def bench_config(a):
     from paper_2411_04776_b200 import synthetic
 
     cfg, n, params, shear, twist = synthetic.workload(a.config, a.seed, a.envs or None)
-    over = dict(lut_dtype=a.lut_dtype, kernel_path=a.kernel_path)
+    over = dict(lut_dtype=a.lut_dtype, kernel_path=a.kernel_path, chunk_envs=a.chunk_envs)
     if a.shadows:
         over.update(light_dirs=default_light_dirs(), shadow_factor=0.6)
     return dataclasses.replace(cfg, **over), n, params, shear, twist

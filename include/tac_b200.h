@@ -126,7 +126,8 @@ typedef struct tac_config {
    * arithmetic, except lut_dtype (see TAC_LUT_*). */
   int32_t lut_dtype;                         /* TAC_LUT_* */
   int32_t kernel_path;                       /* TAC_PATH_* */
-  int32_t chunk_envs;                        /* envs per blur/shade launch pair; 0 = 4096 */
+  int32_t chunk_envs;                        /* envs per blur/shade launch pair; 0 = as many as
+                                                fit a 10 GiB blurred scratch */
 } tac_config;
 
 typedef struct tac_ctx tac_ctx;

@@ -38,7 +38,7 @@
 //     (REF/marker.py:103-140), the marker displacements (REF/marker.py:143-165)
 //     and the dot splat (REF/marker.py:203-234).
 //
-// Envs run in chunks of tac_config.chunk_envs (default 4096): smaller chunks keep the
+// Envs run in chunks of tac_config.chunk_envs (default: a 10 GiB blurred scratch): smaller chunks keep the
 // blurred intermediate in L2 but measured slower (launch tails dominate).
 #include <climits>
 #include <cuda_fp16.h>
