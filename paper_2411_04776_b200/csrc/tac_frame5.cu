@@ -55,6 +55,9 @@ constexpr int BH = 16;    // band rows
 constexpr int K1T = 320;  // blur threads: 8 row pairs x 40 chunks of 8 columns (W = 320)
 constexpr int K2T = 320;     // shade threads per CTA, at most
 constexpr int K2_MIN = 160;  // preferred smallest shade CTA (measured: 160 > 320 > 640 threads at W = 320)
+struct ShadeCta {
+  int rows, row;  // rows per CTA, threads per row
+};
 #ifndef TAC_SHADE_ROW_ITERS
 #define TAC_SHADE_ROW_ITERS 8
 #endif
@@ -519,17 +522,21 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
   return true;
 }
 
-// One 4-pixel group of one row per thread.  grid (row groups, envs); block (W/4, rpc).
+// One 4-pixel group of one row per thread.  grid (row groups, envs); block
+// (row threads, rows): row threads = W/4, or W/4 rounded up (idle threads at
+// the end of each row) when no row count makes the CTA whole warps.
 #ifndef TAC_K2_MINB
 #define TAC_K2_MINB 4
 #endif
-template <bool H16>
+// PAD: rows padded (a separate instantiation: the extra idle test costs the
+// unpadded kernel registers at its 48-register cap).
+template <bool H16, bool PAD>
 __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __grid_constant__ FrameParams p) {
   const int W = p.W, H = p.H;
   const long long env = blockIdx.y;
   const int gi = threadIdx.x;
-  const int ng = blockDim.x;  // 4-pixel groups per row
   const int xg = 4 * gi;
+  const int ng = blockDim.x;  // threads per row
   const long long HW = (long long)H * W;
   const int lane = (threadIdx.y * ng + gi) & 31;
   const float* img = p.scratch + env * HW + xg;
@@ -541,8 +548,8 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
 #pragma unroll kShadeUnroll
   for (int it = 0; it < kShadeRowIters; ++it) {
     const int y = (blockIdx.x * kShadeRowIters + it) * blockDim.y + threadIdx.y;
-    if (__all_sync(0xffffffffu, y >= H)) break;  // warps hold whole rows: uniform per warp
-    const bool act = y < H;
+    const bool act = y < H && (!PAD || xg < W);  // xg >= W: row padding, idle
+    if (__all_sync(0xffffffffu, !act)) break;  // uniform per warp
     const int yc = act ? y : H - 1;
     const float* rc = img + (long long)yc * W;
     // columns whose gradient can be non-zero: band extents of rows y-1..y+1
@@ -568,7 +575,7 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
     bool done = false;
     if (any) {
       if (lane == 0 || gi == 0) left = xg > 0 ? rc[-1] : cc.x;
-      if (lane == 31 || gi == ng - 1) right = xg + 4 < W ? rc[4] : cc.w;
+      if (lane == 31 || (PAD ? xg + 4 == W : gi == ng - 1)) right = xg + 4 < W ? rc[4] : cc.w;
       const float c[6] = {left, cc.x, cc.y, cc.z, cc.w, right};
       done = shade_group<H16>(p, env, yc, xg, c, mm, nn, out, nsat);
     }
@@ -643,15 +650,25 @@ size_t band_blur_smem_bytes(const FrameParams& p) {
   return sizeof(float) * ((size_t)(BH + 2 * p.R) * p.in_pitch + (size_t)BH * p.v_pitch);
 }
 
-// Rows per shade CTA: whole warps (the row-neighbour shuffles), the smallest
-// such CTA of at least K2_MIN threads, at most K2T; 0 if none.
-int shade_rows_per_cta(int ng) {
-  int r0 = 1;
-  while ((ng * r0) % 32 != 0) ++r0;
-  if (ng * r0 > K2T) return 0;
-  int r = r0;
-  while (ng * r < K2_MIN && ng * (r + r0) <= K2T) r += r0;
-  return r;
+// Shade CTA shape: rows of `row` threads (W/4, or W/4 rounded up to the
+// next multiple of 8 / 16 / 32) so that row x rows is whole warps, at most
+// K2T threads; the fewest padded threads first, then the smallest CTA of at
+// least K2_MIN threads.  rows = 0 if none fits.
+ShadeCta shade_cta(int ng) {
+  ShadeCta c{0, 0};
+  if (ng <= 0) return c;
+  for (int al = 1; al <= 32 && c.rows == 0; al *= 2) {
+    const int row = (ng + al - 1) / al * al;
+    if (row > K2T) break;
+    int r0 = 1;
+    while ((row * r0) % 32 != 0) ++r0;
+    if (row * r0 > K2T) continue;
+    int r = r0;
+    while (row * r < K2_MIN && row * (r + r0) <= K2T) r += r0;
+    c.rows = r;
+    c.row = row;
+  }
+  return c;
 }
 
 bool frame5_eligible(const FrameParams& p) {
@@ -661,7 +678,7 @@ bool frame5_eligible(const FrameParams& p) {
   if (p.lut_tex == 0) return false;  // the shade kernel reads LUT plane 1 through a texture
   const int ng = p.W / 4;
   if ((ng * (K1T / ng)) % 32 != 0) return false;  // whole warps (shuffles, block_reduce)
-  if (shade_rows_per_cta(ng) == 0) return false;
+  if (shade_cta(ng).rows == 0) return false;
   return band_blur_smem_bytes(p) <= 227 * 1024;
 }
 
@@ -670,7 +687,7 @@ bool shade5_eligible(const FrameParams& p) {
   if (p.W % 16 != 0 || p.W < 16) return false;
   if (p.mg.rows * p.mg.cols > 1024) return false;
   if (p.lut_tex == 0) return false;
-  return shade_rows_per_cta(p.W / 4) != 0;
+  return shade_cta(p.W / 4).rows != 0;
 }
 
 int frame5_launches(const FrameParams& p, long long n_env) {
@@ -688,8 +705,9 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm, cons
   const long long HW = (long long)p0.H * p0.W;
   const int ng = p0.W / 4;
   const dim3 b1(ng, K1T / ng);
-  const int rpc = shade_rows_per_cta(ng);
-  const dim3 b2(ng, rpc);
+  const ShadeCta sc = shade_cta(ng);
+  const int rpc = sc.rows;
+  const dim3 b2(sc.row, rpc);
   const unsigned nq = (unsigned)((p0.H + rpc * kShadeRowIters - 1) / (rpc * kShadeRowIters));
   const long long chunk = p0.chunk > 0 ? p0.chunk : p0.n_env;
   const long long nchunks = (p0.n_env + chunk - 1) / chunk;
@@ -724,10 +742,16 @@ cudaError_t launch_frame5(const FrameParams& p0, cudaStream_t s, Marks* tm, cons
       CK(cudaGetLastError());
     }
     tm->mark(0);
-    if (p.lut_h16)
-      band_shade_kernel<true><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
-    else
-      band_shade_kernel<false><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    if (sc.row != ng) {
+      if (p.lut_h16)
+        band_shade_kernel<true, true><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+      else
+        band_shade_kernel<false, true><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    } else if (p.lut_h16) {
+      band_shade_kernel<true, false><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    } else {
+      band_shade_kernel<false, false><<<dim3(nq, (unsigned)n), b2, 0, s>>>(p);
+    }
     CK(cudaGetLastError());
     tm->mark(1);
   }

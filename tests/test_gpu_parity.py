@@ -925,3 +925,19 @@ def test_pipeline_saturation_count_matches_standalone_shade():
     assert torch.equal(obs.saturated.cpu(), sat.cpu())
     assert int(sat.sum()) > 0
     assert torch.equal(obs.summary[:, 7].cpu(), sat.float().cpu())
+
+
+@pytest.mark.parametrize("hw", [(37, 480), (24, 1024), (50, 336), (29, 400)])
+def test_stream_path_column_strips(hw):
+    """The row-streaming blur's column strips (W > 320: strips of <= 320
+    output columns with R4-column halos), ragged heights, sigma 1,2,4; the
+    shade kernel's padded rows (W/4 = 120, 84, 100: no whole-warp CTA
+    without idle threads)."""
+    h, w = hw
+    cfg = small_config(h, w, grid=(3, 5))
+    assert TactilePipeline(cfg, DEV).path_name() == "stream"
+    depth = depth_batch(3, h, w, seed=101)
+    shear, twist = synthetic.loads(3, 102)
+    obs = run_pipeline(cfg, depth, shear, twist)
+    for i in range(3):
+        check_env(cfg, depth[i].numpy(), obs, i, shear[i], twist[i])

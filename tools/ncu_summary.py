@@ -50,7 +50,7 @@ lines, traffic = [], {}
 for vals in rows[2:]:
     d = {n: (vals[i], units[i]) for i, n in enumerate(h)}
     name = d["Kernel Name"][0]
-    m = re.search(r"(\w+_kernel)(<(\w+)>)?", name)
+    m = re.search(r"(\w+_kernel)(<(\w+)[,>])?", name)
     short = m.group(1) if m else name
     if short == "band_shade_kernel" and m.group(3) in ("true", "1"):
         short = "band_shade_kernel<f16 LUT>"
