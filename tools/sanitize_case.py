@@ -14,8 +14,16 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(
 from _helpers import depth_batch, small_config  # noqa: E402
 from paper_2411_04776_b200 import TactilePipeline, render_heightmaps, synthetic  # noqa: E402
 
-for (h, w, n) in ((240, 320, 3), (48, 64, 2)):
-    cfg = synthetic.baseline_config(2, 0)[0] if (h, w) == (240, 320) else small_config(h, w)
+import dataclasses  # noqa: E402
+
+cases = [(synthetic.baseline_config(2, 0)[0], 3),            # stream blur, sigma 1,2,4
+         (small_config(48, 64), 2),
+         (small_config(37, 480, grid=(3, 5)), 2),             # column strips, padded shade rows
+         (small_config(48, 64, shadows=True), 2),             # tiled shadow march, stream path
+         (dataclasses.replace(small_config(48, 64), lut_dtype="f16"), 2),
+         (small_config(40, 56, shadows=True), 2)]             # L1 shadow march + fused-path fallback
+for cfg, n in cases:
+    h, w = cfg.sensor.image_size
     pipe = TactilePipeline(cfg, "cuda")
     d = depth_batch(n, h, w, seed=3).cuda()
     sh, tw = synthetic.loads(n, 4)
