@@ -53,7 +53,10 @@ namespace {
 
 constexpr int BH = 16;    // band rows
 constexpr int K1T = 320;  // blur threads: 8 row pairs x 40 chunks of 8 columns (W = 320)
-constexpr int K2T = 320;     // shade threads per CTA, at most
+#ifndef TAC_K2T
+#define TAC_K2T 320
+#endif
+constexpr int K2T = TAC_K2T;  // shade threads per CTA, at most
 constexpr int K2_MIN = 160;  // preferred smallest shade CTA (measured: 160 > 320 > 640 threads at W = 320)
 struct ShadeCta {
   int rows, row;  // rows per CTA, threads per row
@@ -381,13 +384,95 @@ __device__ __forceinline__ void ld256u(const void* p, uint32_t (&w)[8]) {
 __device__ __forceinline__ float h2f_lo(uint32_t w) { return __half2float(__ushort_as_half((unsigned short)(w & 0xffffu))); }
 __device__ __forceinline__ float h2f_hi(uint32_t w) { return __half2float(__ushort_as_half((unsigned short)(w >> 16))); }
 
-// add_lut with the bin's 15 coefficients stored as fp16 (lut_dtype f16):
-// halfs [R c1..c5, G c1..c5, B c1..c5, pad], same operation order as add_lut
-__device__ __forceinline__ void add_lut_h(const uint32_t (&w)[8], float nx, float ny, float& r, float& g, float& b) {
-  const float nxx = nx * nx, nxy = nx * ny, nyy = ny * ny;
-  r += h2f_lo(w[0]) * nx + h2f_hi(w[0]) * ny + h2f_lo(w[1]) * nxx + h2f_hi(w[1]) * nxy + h2f_lo(w[2]) * nyy;
-  g += h2f_hi(w[2]) * nx + h2f_lo(w[3]) * ny + h2f_hi(w[3]) * nxx + h2f_lo(w[4]) * nxy + h2f_hi(w[4]) * nyy;
-  b += h2f_lo(w[5]) * nx + h2f_hi(w[5]) * ny + h2f_lo(w[6]) * nxx + h2f_hi(w[6]) * nxy + h2f_lo(w[7]) * nyy;
+// ---- paired binning (two pixels per fp32x2 op) ----------------------------------
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// Bins of two pixels and their normals' (x, y) NEGATED: m = (gx, gy) / sqrt(1 + |g|^2)
+// = -(n_x, n_y) (the shading negates the linear terms).  Same definitions as
+// bin_px: magnitude bin min(floor(|g| mag_scale), bins - 1),
+// direction bin floor((atan2(gy, gx) + pi) dir_scale) mod bins, both 0 for a
+// zero gradient (NaN converts to 0).  i = direction-major planar bin index.
+struct Bins2 {
+  float2 nx, ny;
+  int i0, i1;
+};
+
+__device__ __forceinline__ int dir_fix(int db, int bins) {
+  db = db >= bins ? db - bins : db;
+  return max(db, 0);
+}
+
+__device__ __forceinline__ Bins2 bin_pair(const FrameParams& p, float2 gx, float2 gy) {
+  Bins2 o;
+  const float2 g2 = ffma2(gx, gx, f2mul(gy, gy));
+  const float2 gm = f2mul(g2, make_float2(rsqrtf(g2.x), rsqrtf(g2.y)));  // NaN for g2 == 0 -> bin 0
+  const float2 t = f2add(g2, bc2(1.f));
+  const float2 inv = make_float2(rsqrtf(t.x), rsqrtf(t.y));
+  o.nx = f2mul(gx, inv);
+  o.ny = f2mul(gy, inv);
+  const float2 ms = f2mul(gm, bc2(p.mag_scale));
+  // atan2 by an odd minimax polynomial of min/max on [0, 1] (|err| ~ 1e-7 rad) + reflections
+  const float ax0 = fabsf(gx.x), ay0 = fabsf(gy.x), ax1 = fabsf(gx.y), ay1 = fabsf(gy.y);
+  const float2 mn = make_float2(fminf(ax0, ay0), fminf(ax1, ay1));
+  const float2 mx = make_float2(fmaxf(ax0, ay0), fmaxf(ax1, ay1));
+  const float2 a = f2mul(mn, make_float2(rcp_approx(mx.x), rcp_approx(mx.y)));  // 0/0 -> NaN -> bin 0
+  const float2 s = f2mul(a, a);
+  float2 q = bc2(0.0024567204527556896f);
+  q = ffma2(q, s, bc2(-0.01440134271979332f));
+  q = ffma2(q, s, bc2(0.039781197905540466f));
+  q = ffma2(q, s, bc2(-0.07234855741262436f));
+  q = ffma2(q, s, bc2(0.10498945415019989f));
+  q = ffma2(q, s, bc2(-0.14161229133605957f));
+  q = ffma2(q, s, bc2(0.19985906779766083f));
+  q = ffma2(q, s, bc2(-0.33332598209381104f));
+  q = ffma2(q, s, bc2(0.9999998807907104f));
+  float2 r = f2mul(q, a);
+  r.x = (ay0 > ax0) ? kHalfPi - r.x : r.x;
+  r.y = (ay1 > ax1) ? kHalfPi - r.y : r.y;
+  r.x = (gx.x < 0.f) ? kPi - r.x : r.x;
+  r.y = (gx.y < 0.f) ? kPi - r.y : r.y;
+  r.x = (gy.x < 0.f) ? -r.x : r.x;
+  r.y = (gy.y < 0.f) ? -r.y : r.y;
+  const float2 u = f2mul(f2add(r, bc2(kPi)), bc2(p.dir_scale));
+  const int mb0 = max(min((int)ms.x, p.mag_bins - 1), 0), mb1 = max(min((int)ms.y, p.mag_bins - 1), 0);
+  const int db0 = dir_fix((int)u.x, p.dir_bins), db1 = dir_fix((int)u.y, p.dir_bins);
+  o.i0 = db0 * p.mag_bins + mb0;  // direction-major (tac_ctx_create)
+  o.i1 = db1 * p.mag_bins + mb1;
+  return o;
+}
+
+// bg + Delta_c (REF/optical.py:82-88, :244) with the bin's 15 coefficients as
+// fp16 [R c1..c5, G c1..c5, B c1..c5, pad], one FMA chain per channel, (mx, my)
+// = -(nx, ny): the linear terms' coefficients are negated in the FMA.
+__device__ __forceinline__ void shade_h(const uint32_t (&w)[8], float mx, float my, float xx, float xy, float yy,
+                                        const float* bg, float (&o)[3]) {
+  o[0] = fmaf(h2f_lo(w[2]), yy, fmaf(h2f_hi(w[1]), xy, fmaf(h2f_lo(w[1]), xx,
+         fmaf(-h2f_hi(w[0]), my, fmaf(-h2f_lo(w[0]), mx, bg[0])))));
+  o[1] = fmaf(h2f_hi(w[4]), yy, fmaf(h2f_lo(w[4]), xy, fmaf(h2f_hi(w[3]), xx,
+         fmaf(-h2f_lo(w[3]), my, fmaf(-h2f_hi(w[2]), mx, bg[1])))));
+  o[2] = fmaf(h2f_lo(w[7]), yy, fmaf(h2f_hi(w[6]), xy, fmaf(h2f_lo(w[6]), xx,
+         fmaf(-h2f_hi(w[5]), my, fmaf(-h2f_lo(w[5]), mx, bg[2])))));
 }
 
 __device__ __forceinline__ int planar_bin(const FrameParams& p, int mb, int db) {
@@ -452,24 +537,23 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
     const float4 f4 = __ldg(reinterpret_cast<const float4*>(p.shadow + env * HW + (long long)y * W + xg));
     sf[0] = f4.x; sf[1] = f4.y; sf[2] = f4.z; sf[3] = f4.w;
   }
-  uint32_t qb[12];
+  uint32_t qb[12], w01 = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
-    const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
-    // two 256-bit loads per pixel: floats 0..7 and 8..15 of the bin
-    const int i0 = planar_bin(p, a0p.mb, a0p.db);
-    const int i1 = planar_bin(p, a1p.mb, a1p.db);
     if constexpr (H16) {
-      // fp16 LUT: one 32-B sector per bin (half the gather bytes)
+      // pixels 2h, 2h+1 binned together (paired fp32 ops); fp16 LUT: one
+      // 32-B sector per bin (half the gather bytes)
+      const Bins2 bq = bin_pair(p, make_float2(gxs[2 * h], gxs[2 * h + 1]), make_float2(gys[2 * h], gys[2 * h + 1]));
+      const float2 nxx = f2mul(bq.nx, bq.nx), nxy = f2mul(bq.nx, bq.ny), nyy = f2mul(bq.ny, bq.ny);
       uint32_t w0[8], w1[8];
-      ld256u(p.lut_h16 + 2 * i0, w0);
-      ld256u(p.lut_h16 + 2 * i1, w1);
+      ld256u(p.lut_h16 + 2 * bq.i0, w0);
+      ld256u(p.lut_h16 + 2 * bq.i1, w1);
+      float rgb[2][3];
+      shade_h(w0, bq.nx.x, bq.ny.x, nxx.x, nxy.x, nyy.x, &bgv[6 * h], rgb[0]);
+      shade_h(w1, bq.nx.y, bq.ny.y, nxx.y, nxy.y, nyy.y, &bgv[6 * h + 3], rgb[1]);
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const Px& pp = s ? a1p : a0p;
-        float r = bgv[6 * h + 3 * s], g = bgv[6 * h + 3 * s + 1], b = bgv[6 * h + 3 * s + 2];
-        add_lut_h(s ? w1 : w0, pp.nx, pp.ny, r, g, b);
+        float r = rgb[s][0], g = rgb[s][1], b = rgb[s][2];
         if (p.saturated) nsat += clip_count(r, g, b);
         if (p.shadow) {
           const float f = sf[2 * h + s];
@@ -481,8 +565,16 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
         qb[6 * h + 3 * s + 1] = u8sat(g);
         qb[6 * h + 3 * s + 2] = u8sat(b);
       }
+      if (h == 0) w01 = pack4(qb[0], qb[1], qb[2], qb[3]);  // pixels 0, 1 done: fewer live registers
       continue;
     }
+    // fp32 LUT (16 coefficients per pixel in registers): per-pixel binning
+    // (the paired form exceeds the 48-register cap here: spills, measured 3 % slower)
+    const Px a0p = bin_px(p, gxs[2 * h], gys[2 * h]);
+    const Px a1p = bin_px(p, gxs[2 * h + 1], gys[2 * h + 1]);
+    // two 256-bit loads per pixel: floats 0..7 and 8..15 of the bin
+    const int i0 = planar_bin(p, a0p.mb, a0p.db);
+    const int i1 = planar_bin(p, a1p.mb, a1p.db);
     float4 a0, c0, d0, e0, a1, c1, d1, e1;
     {
       // plane 0 through the LSU (256-bit), plane 1 through the texture path:
@@ -516,7 +608,7 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
     }
   }
   uint32_t* d = reinterpret_cast<uint32_t*>(out + ((long long)y * W + xg) * 3);
-  d[0] = pack4(qb[0], qb[1], qb[2], qb[3]);
+  d[0] = H16 ? w01 : pack4(qb[0], qb[1], qb[2], qb[3]);
   d[1] = pack4(qb[4], qb[5], qb[6], qb[7]);
   d[2] = pack4(qb[8], qb[9], qb[10], qb[11]);
   return true;
