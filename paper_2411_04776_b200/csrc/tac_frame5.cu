@@ -693,14 +693,16 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
 __global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant__ FrameParams p) {
   __shared__ double s_dbl[8];
   __shared__ int s_int[2 * 1024];
+  __shared__ int s_recount;
+  __shared__ unsigned s_nf;
   const long long env = blockIdx.x;
   const int nb = p.nparts;
+  double cnt = 0, sw = 0, swx = 0, swy = 0, nf = 0;  // folded by warp 0 (thread 0 finalises)
+  float mx = 0.f;
   if (threadIdx.x < 32) {
     // warp 0: lane s folds bands s, s + 32, ...; then a fixed xor butterfly
     // (every lane ends with the same bits: deterministic for a given band count)
     const int lane = threadIdx.x;
-    double cnt = 0, sw = 0, swx = 0, swy = 0, nf = 0;
-    float mx = 0.f;
     const double* q = p.partials + env * nb * kSumFields;
     for (int s = lane; s < nb; s += 32) {
       cnt += q[s * 8 + 0];
@@ -719,8 +721,22 @@ __global__ void __launch_bounds__(128) env_epilogue_kernel(const __grid_constant
       nf += __shfl_xor_sync(0xffffffffu, nf, o);
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    if (lane == 0) finalize_load(p, env, cnt, sw, swx, swy, mx, nf, s_dbl);
+    if (lane == 0) s_recount = nf < 0.0 ? 1 : 0;
+    s_nf = 0u;
   }
+  __syncthreads();
+  if (s_recount) {
+    // a stream-blur strip flagged a non-finite raw value (tac_stream.cu):
+    // count this env's non-finite inputs exactly (integer sum: deterministic)
+    const float* in = p.in + env * (long long)p.H * p.W;
+    unsigned c = 0;
+    for (long long i = threadIdx.x; i < (long long)p.H * p.W; i += blockDim.x) c += fabsf(in[i]) < INFINITY ? 0u : 1u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_nf, c);
+    __syncthreads();
+    nf = (double)s_nf;
+  }
+  if (threadIdx.x == 0) finalize_load(p, env, cnt, sw, swx, swy, mx, nf, s_dbl);
   __syncthreads();
   if (p.finalize != 2) return;
   const Load l = load_from(s_dbl);

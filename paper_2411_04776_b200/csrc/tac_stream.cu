@@ -106,26 +106,40 @@ __device__ __forceinline__ void bar_arrive_n(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// The H item's window of non-zero flags: column pairs [qa, qb] of the V
+// range (the widest level's taps around the item's 8 columns) lie in the
+// bitmask words w and w + 1 (a window spans <= 2 R4 + 8 <= 56 columns, 28
+// pairs); the item is non-zero if (nzs[w] & lo) | (nzs[w + 1] & hi).
+struct HWin {
+  int w;
+  uint32_t lo, hi;
+};
+template <class PY>
+__device__ __forceinline__ HWin h_window(int c0, int vx0, int npairs) {
+  constexpr int R4 = PY::R4;
+  static_assert(2 * R4 + 8 <= 64, "an H window spans at most two bitmask words");
+  const int qa = max((c0 - R4 - vx0) >> 1, 0);
+  const int qb = min((c0 + 8 + R4 - vx0) >> 1, npairs) - 1;
+  HWin h;
+  h.w = qa >> 5;
+  const int a = qa & 31, b = max(qb - 32 * h.w, a);  // b in [a, 63]
+  h.lo = (~0u << a) & (b >= 31 ? ~0u : ~0u >> (31 - b));
+  h.hi = b >= 32 ? ~0u >> (63 - b) : 0u;
+  return h;
+}
+
 // One H item: row pair m x 8 columns (acc[i] = (row 2m, row 2m+1) at column
 // c0 + i) from the V block slot `vs` (column index 0 = global column vx0 - R4).
 // Returns false (acc = 0) when the V window of the widest level is all zero.
 template <class PY, class G>
 __device__ __forceinline__ bool h_item(const FrameParams& p, const float* vs, const uint32_t* nzs, int m, int c0,
-                                       int vx0, int npairs, float2 (&acc)[8]) {
+                                       int vx0, const HWin& hw, float2 (&acc)[8]) {
   constexpr int L = PY::L, R4 = PY::R4;
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
-  const int qa = max((c0 - R4 - vx0) >> 1, 0);
-  const int qb = min((c0 + 8 + R4 - vx0) >> 1, npairs) - 1;
-  bool any = false;
-  for (int w = qa >> 5; w <= (qb >> 5); ++w) {
-    uint32_t bits = nzs[w];
-    const int b0 = w * 32;
-    if (qa > b0) bits &= ~0u << (qa - b0);
-    if (qb < b0 + 31) bits &= ~0u >> (b0 + 31 - qb);
-    any |= bits != 0u;
-  }
-  if (!any) return false;
+  // (hi == 0 when the window ends in word w: word w + 1 is then not read)
+  const uint32_t bits = (nzs[hw.w] & hw.lo) | (hw.hi ? nzs[hw.w + 1] & hw.hi : 0u);
+  if (bits == 0u) return false;
   // row pair m at column c0 - R4 (16-B aligned: every offset is a multiple of 4 columns)
   const float* base = vs + m * G::RPP + 2 * (c0 - vx0);
 #pragma unroll
@@ -232,7 +246,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     const bool partials = p.finalize != 0 && own;
     const double yoff = 0.5 - (double)p.half_h;
     float cnt = 0.f, mx = 0.f;
-    int nf = 0;
+    float2 probe = make_float2(0.f, 0.f);  // sum of the raw values read (non-finite flag)
     float cs0 = 0.f, cs1 = 0.f;  // fp32 column sums of the current input block
     double sw = 0.0, swx = 0.0, swy = 0.0;
     float2 win[P];
@@ -249,9 +263,11 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         v.y = clampf(v.y, 0.f, p.rest);
       }
       const bool nzw = __any_sync(0xffffffffu, (__float_as_uint(v.x) | __float_as_uint(v.y)) != 0u);
-      // raw non-finite values clamp to 0; count them (summary field 6)
-      if (!(fabsf(raw.x + raw.y) < INFINITY) && partials && y < H)
-        nf += (fabsf(raw.x) < INFINITY ? 0 : 1) + (fabsf(raw.y) < INFINITY ? 0 : 1);
+      // raw non-finite values clamp to 0 or rest; a running sum of the raw
+      // values becomes non-finite if any is (or on a finite overflow): the
+      // strip then flags its env and the epilogue counts them exactly
+      // (summary field 6) -- one FADD2 per row instead of a per-row count
+      probe = fadd2(probe, raw);
       if (nzw) {
         last_nz = y;
         if (partials && y < H) {
@@ -381,7 +397,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     Red red;
     red.cnt = cnt;
     red.mx = mx;
-    red.nf = (float)nf;
+    red.nf = (partials && !(fabsf(probe.x + probe.y) < INFINITY)) ? -1.f : 0.f;  // < 0: recount
     red.sw = sw;
     red.swx = swx;
     red.swy = swy;
@@ -415,6 +431,9 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     const int nht = 32 * nhw;
     const int nitems = 4 * ((x1 - x0) >> 3);
     const int npairs = (vx1 - vx0) >> 1;
+    // the (<= 2) items of this lane and their window masks (the same every block)
+    const HWin hw0 = h_window<PY>(x0 + 8 * (ht >> 2), vx0, npairs);
+    const HWin hw1 = h_window<PY>(x0 + 8 * ((ht + nht) >> 2), vx0, npairs);
     int lo = INT_MAX, hi = INT_MIN;  // non-zero output columns of the current band
     int next_issue = min(NS, nblk_in);  // (H thread 0) next input block to stream
     bar_arrive_n(kBarEmpty + 0, nthreads);
@@ -435,7 +454,8 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         const int m = item & 3;
         const int c0 = x0 + 8 * (item >> 2);
         float2 acc[8];
-        const bool any = h_item<PY, G>(p, vs, s_nz + (sv * (SB / 2) + m) * kMaxVW, m, c0, vx0, npairs, acc);
+        const bool any =
+            h_item<PY, G>(p, vs, s_nz + (sv * (SB / 2) + m) * kMaxVW, m, c0, vx0, item == ht ? hw0 : hw1, acc);
         const int y = SB * j + 2 * m;
         float* d = p.scratch + env * HW + (long long)y * W + c0;
         if (y < H) {

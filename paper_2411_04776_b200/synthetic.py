@@ -154,7 +154,7 @@ def loads(n, seed):
 
 
 def baseline_config(index, seed=0):
-    """(PipelineConfig, n_env, description) for BASELINE.json configs[index]."""
+    """(PipelineConfig, n_env) for BASELINE.json configs[index]."""
     if index == 3:
         h, w, sig, grid = 480, 640, (1.0, 2.0, 4.0, 8.0), (14, 18)
     else:

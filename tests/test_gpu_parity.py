@@ -186,6 +186,20 @@ class TestPipelineParity:
         assert obs.summary[0, 6].item() == 0
         assert obs.summary[1, 6].item() == 2
 
+    def test_nonfinite_flag_recount_wide_and_overflow(self):
+        """The stream blur flags an env whose raw values sum to a non-finite
+        value and the epilogue recounts it exactly: -inf / NaN in either column
+        strip of a 480x640 frame, and finite values whose sum overflows (a
+        flag with an exact count of 0)."""
+        cfg, _ = synthetic.baseline_config(3, 0)
+        depth = torch.full((3, 480, 640), synthetic.REST, dtype=torch.float32)
+        depth[0, 0, 639] = float("-inf")
+        depth[0, 479, 0] = float("nan")
+        depth[0, 200, 300] = float("inf")
+        depth[1, 10:20, 100] = 3.0e38  # finite; the running sum overflows
+        obs = run_pipeline(cfg, depth, np.zeros((3, 2)), np.zeros(3))
+        assert [obs.summary[i, 6].item() for i in range(3)] == [3, 0, 0]
+
     def test_workspace_reuse_is_deterministic(self):
         cfg = small_config(48, 64)
         depth = depth_batch(5, 48, 64, seed=13)
