@@ -99,6 +99,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return r;
 }
 
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -245,9 +254,10 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     const bool depth_in = p.input_depth != 0;
     const bool partials = p.finalize != 0 && own;
     const double yoff = 0.5 - (double)p.half_h;
-    float cnt = 0.f, mx = 0.f;
+    float mx = 0.f;
+    float2 cnt2 = make_float2(0.f, 0.f);  // contact pixels of the pair's two columns
     float2 probe = make_float2(0.f, 0.f);  // sum of the raw values read (non-finite flag)
-    float cs0 = 0.f, cs1 = 0.f;  // fp32 column sums of the current input block
+    float2 cs = make_float2(0.f, 0.f);  // fp32 column sums of the current input block
     double sw = 0.0, swx = 0.0, swy = 0.0;
     float2 win[P];
     int last_nz = INT_MIN / 2;  // last input row with a non-zero value in the warp's columns (warp-uniform)
@@ -272,11 +282,12 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         last_nz = y;
         if (partials && y < H) {
           mx = fmaxf(mx, fmaxf(v.x, v.y));
-          const float w0 = v.x > thr ? v.x : 0.f, w1 = v.y > thr ? v.y : 0.f;
-          cnt += (v.x > thr ? 1.f : 0.f) + (v.y > thr ? 1.f : 0.f);
-          cs0 += w0;
-          cs1 += w1;
-          const float rs = w0 + w1;
+          // contact mask as 1/0 (v is finite and >= 0: v * 0 = +0, v * 1 = v)
+          const float2 f = make_float2(v.x > thr ? 1.f : 0.f, v.y > thr ? 1.f : 0.f);
+          const float2 w = fmul2(v, f);
+          cnt2 = fadd2(cnt2, f);
+          cs = fadd2(cs, w);
+          const float rs = w.x + w.y;
           sw += (double)rs;
           swy = fma((double)rs, (double)y + yoff, swy);
         }
@@ -284,12 +295,12 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
       return v;
     };
     auto flush_cols = [&]() {
-      if (partials && (cs0 != 0.f || cs1 != 0.f)) {
+      if (partials && (cs.x != 0.f || cs.y != 0.f)) {
         const double xc0 = (double)c + p.xoff;
-        swx = fma((double)cs0, xc0, swx);
-        swx = fma((double)cs1, xc0 + 1.0, swx);
+        swx = fma((double)cs.x, xc0, swx);
+        swx = fma((double)cs.y, xc0 + 1.0, swx);
       }
-      cs0 = cs1 = 0.f;
+      cs = make_float2(0.f, 0.f);
     };
 
     // ---- prologue: ring rows -R .. R-1 (rows < 0 replicate row 0) ----------
@@ -395,7 +406,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     // ---- contact partials of the strip: V warps only ----------------------------
     if (p.finalize == 0) return;
     Red red;
-    red.cnt = cnt;
+    red.cnt = cnt2.x + cnt2.y;
     red.mx = mx;
     red.nf = (partials && !(fabsf(probe.x + probe.y) < INFINITY)) ? -1.f : 0.f;  // < 0: recount
     red.sw = sw;
