@@ -48,7 +48,6 @@ constexpr int kMaxStrip = 320;  // output columns per CTA
 constexpr int kBarFull = 1;   // + block parity
 constexpr int kBarEmpty = 3;  // + block parity
 constexpr int kBarV = 5;
-constexpr int kBarH = 6;
 
 template <int L_, int R0, int R1 = 0, int R2 = 0, int R3 = 0>
 struct Pyr {
@@ -85,9 +84,8 @@ struct Geo5 {
   static constexpr size_t NZ_OFF = VB_OFF + (size_t)2 * VSLOT * 4;
   static constexpr size_t RED_OFF = NZ_OFF + (size_t)2 * (SB / 2) * kMaxVW * 4;
   static constexpr size_t BAR_OFF = RED_OFF + (size_t)kMaxVW * 8 * 8;
-  static constexpr size_t EXT_OFF = BAR_OFF + (size_t)PY::NS * 8;
-  // + nbands * nhw int2 (runtime)
-  static size_t bytes(int nbands, int nhw) { return (EXT_OFF + (size_t)nbands * nhw * 8 + 127) & ~size_t(127); }
+  static constexpr size_t END = BAR_OFF + (size_t)PY::NS * 8;
+  static size_t bytes(int, int) { return (END + 127) & ~size_t(127); }
 };
 
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
@@ -225,7 +223,6 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
   uint32_t* s_nz = reinterpret_cast<uint32_t*>(smem_raw + G::NZ_OFF);
   double* s_red = reinterpret_cast<double*>(smem_raw + G::RED_OFF);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(smem_raw + G::BAR_OFF);
-  int2* s_ext = reinterpret_cast<int2*>(smem_raw + G::EXT_OFF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* src = p.in + env * HW;
 
@@ -438,14 +435,12 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     // items = (row pair m, 8-column chunk) of a block; lane ht takes items ht
     // and ht + 32 nhw (the same chunks in every block)
     const int ht = threadIdx.x - 32 * nvw;
-    const int hw = warp - nvw;
     const int nht = 32 * nhw;
     const int nitems = 4 * ((x1 - x0) >> 3);
     const int npairs = (vx1 - vx0) >> 1;
     // the (<= 2) items of this lane and their window masks (the same every block)
     const HWin hw0 = h_window<PY>(x0 + 8 * (ht >> 2), vx0, npairs);
     const HWin hw1 = h_window<PY>(x0 + 8 * ((ht + nht) >> 2), vx0, npairs);
-    int lo = INT_MAX, hi = INT_MIN;  // non-zero output columns of the current band
     int next_issue = min(NS, nblk_in);  // (H thread 0) next input block to stream
     bar_arrive_n(kBarEmpty + 0, nthreads);
     if (nblk > 1) bar_arrive_n(kBarEmpty + 1, nthreads);
@@ -465,8 +460,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         const int m = item & 3;
         const int c0 = x0 + 8 * (item >> 2);
         float2 acc[8];
-        const bool any =
-            h_item<PY, G>(p, vs, s_nz + (sv * (SB / 2) + m) * kMaxVW, m, c0, vx0, item == ht ? hw0 : hw1, acc);
+        h_item<PY, G>(p, vs, s_nz + (sv * (SB / 2) + m) * kMaxVW, m, c0, vx0, item == ht ? hw0 : hw1, acc);
         const int y = SB * j + 2 * m;
         float* d = p.scratch + env * HW + (long long)y * W + c0;
         if (y < H) {
@@ -477,30 +471,8 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
           reinterpret_cast<float4*>(d + W)[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
           reinterpret_cast<float4*>(d + W)[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
         }
-        if (any) {
-          lo = min(lo, c0);
-          hi = max(hi, c0 + 7);
-        }
       }
       if (j + 2 < nblk) bar_arrive_n(kBarEmpty + sv, nthreads);
-      // band (16 rows = 2 blocks) complete: per-warp extent
-      if ((j & 1) || j == nblk - 1) {
-        const int blo = __reduce_min_sync(0xffffffffu, lo);
-        const int bhi = __reduce_max_sync(0xffffffffu, hi);
-        if (lane == 0) s_ext[(j >> 1) * nhw + hw] = make_int2(blo, bhi);
-        lo = INT_MAX;
-        hi = INT_MIN;
-      }
-    }
-    bar_sync_n(kBarH, nht);
-    for (int b = ht; b < nbands; b += nht) {
-      int2 e = make_int2(INT_MAX, INT_MIN);
-      for (int w = 0; w < nhw; ++w) {
-        const int2 x = s_ext[b * nhw + w];
-        e.x = min(e.x, x.x);
-        e.y = max(e.y, x.y);
-      }
-      p.band_ext[(env * nbands + b) * p.ext_strips + strip] = e;
     }
   }
 }
