@@ -19,9 +19,11 @@
 //            block [level][row pair][column] with rows interleaved in pairs,
 //            plus a per-row-pair bitmask of the non-zero column pairs.
 //            Replicate borders: rows outside the frame are copies of the
-//            edge row (ring fill); the warp holding an edge column writes the
-//            column pads cooperatively (one float4 per lane).
-//   H warps  one (row pair, 8 columns) item per lane and block, <= 2 items
+//            edge row (ring fill); columns outside it are pads that the last
+//            H warp writes (below): the V warps are the critical path.
+//   H warps  the last H warp first writes the block's replicate column pads
+//            (then an H-only named barrier); one (row pair, 8 columns) item
+//            per lane and block, <= 2 items
 //            per lane: the item's window of each level is loaded into
 //            registers (LDS.128, every FFMA2 operand one aligned float2 of
 //            the interleaved block) and convolved tap-outer, summed over the
@@ -47,6 +49,7 @@ constexpr int kMaxStrip = 320;  // output columns per CTA
 // barrier ids (0 = __syncthreads)
 constexpr int kBarFull = 1;   // + block parity
 constexpr int kBarEmpty = 3;  // + block parity
+constexpr int kBarPad = 6;    // H warps: replicate pads written
 constexpr int kBarV = 5;
 
 template <int L_, int R0, int R1 = 0, int R2 = 0, int R3 = 0>
@@ -243,9 +246,6 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     const bool own = act && c >= x0 && c < x1;  // counted in this strip's contact partials
     const float* col = in_s + (cr - vx0);
     float* vcol = vb + 2 * (c - vx0 + R4);  // the pair's float4 in row pair 0, level 0, slot 0
-    // the warps holding frame-edge columns write the column pads (warp-uniform)
-    const bool padl_w = vx0 == 0 && warp == 0;
-    const bool padr_w = vx1 == W && warp == (((W - 2 - vx0) >> 1) >> 5);
     const float2 rr = make_float2(p.rest, p.rest), rl = make_float2(p.rest_lo, p.rest_lo);
     const float thr = p.threshold;
     const bool depth_in = p.input_depth != 0;
@@ -372,25 +372,6 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
             *reinterpret_cast<float4*>(vs + (l * (SB / 2) + k) * G::RPP) =
                 make_float4(oa[l].x, ob[l].x, oa[l].y, ob[l].y);
         }
-        if (padl_w || padr_w) {
-          // replicate pads: lane t < r4l/2 writes pad float4 t of each
-          // level from the edge column the warp just stored (column 0 /
-          // column W-1, read back after a warp barrier)
-          __syncwarp();
-          float* vrow = vb + sv * G::VSLOT + k * G::RPP;
-#pragma unroll
-          for (int l = 0; l < L; ++l) {
-            float* lrow = vrow + l * (SB / 2) * G::RPP;
-            if (padl_w && lane < PY::r4(l) / 2) {
-              const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * R4);
-              *reinterpret_cast<float4*>(lrow + 2 * (R4 - PY::r4(l) + 2 * lane)) = make_float4(e.x, e.y, e.x, e.y);
-            }
-            if (padr_w && lane < PY::r4(l) / 2) {
-              const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * (W - 1 - vx0 + R4));
-              *reinterpret_cast<float4*>(lrow + 2 * (W - vx0 + R4 + 2 * lane)) = make_float4(e.x, e.y, e.x, e.y);
-            }
-          }
-        }
         const uint32_t bal = __ballot_sync(0xffffffffu, act && nz);
         if (lane == 0) nzs[k * kMaxVW] = bal;
       }
@@ -453,6 +434,31 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         const int lim = min((SB * (j + 1) + R) / SB + NS, nblk_in);
         if (next_issue < lim)
           next_issue = stream_refill(src, in_s, s_full, next_issue, lim, NS, G::IP, H, W, vx0, vx1 - vx0);
+      }
+      {
+        // the last H warp writes the block's replicate pads (columns left of
+        // column 0 / right of column W-1, every level and row pair) from the
+        // edge columns the V warps stored; the H warps then sync among
+        // themselves (the V warps, the critical path, do no pad work)
+        if (warp == nvw + nhw - 1 && (vx0 == 0 || vx1 == W)) {
+          float* vblk = vb + sv * G::VSLOT;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const int np = PY::r4(l) / 2;  // float4 pads per side and row pair
+            for (int i = lane; i < 4 * 2 * np; i += 32) {
+              const int k = i / (2 * np), rem = i - k * 2 * np, side = rem >= np ? 1 : 0, t = rem - side * np;
+              float* lrow = vblk + (l * (SB / 2) + k) * G::RPP;
+              if (side == 0 && vx0 == 0) {
+                const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * R4);
+                *reinterpret_cast<float4*>(lrow + 2 * (R4 - 2 * np + 2 * t)) = make_float4(e.x, e.y, e.x, e.y);
+              } else if (side == 1 && vx1 == W) {
+                const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * (W - 1 - vx0 + R4));
+                *reinterpret_cast<float4*>(lrow + 2 * (W - vx0 + R4 + 2 * t)) = make_float4(e.x, e.y, e.x, e.y);
+              }
+            }
+          }
+        }
+        bar_sync_n(kBarPad, nht);
       }
       const float* vs = vb + sv * G::VSLOT;
 #pragma unroll 1
