@@ -546,6 +546,7 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
       const Bins2 bq = bin_pair(p, make_float2(gxs[2 * h], gxs[2 * h + 1]), make_float2(gys[2 * h], gys[2 * h + 1]));
       const float2 nxx = f2mul(bq.nx, bq.nx), nxy = f2mul(bq.nx, bq.ny), nyy = f2mul(bq.ny, bq.ny);
       uint32_t w0[8], w1[8];
+      TAC_CHECK(bq.i0 >= 0 && bq.i0 < p.nbins && bq.i1 >= 0 && bq.i1 < p.nbins);
       ld256u(p.lut_h16 + 2 * bq.i0, w0);
       ld256u(p.lut_h16 + 2 * bq.i1, w1);
       float rgb[2][3];
@@ -575,6 +576,7 @@ __device__ __forceinline__ bool shade_group(const FrameParams& p, long long env,
     // two 256-bit loads per pixel: floats 0..7 and 8..15 of the bin
     const int i0 = planar_bin(p, a0p.mb, a0p.db);
     const int i1 = planar_bin(p, a1p.mb, a1p.db);
+    TAC_CHECK(i0 >= 0 && i0 < p.nbins && i1 >= 0 && i1 < p.nbins);
     float4 a0, c0, d0, e0, a1, c1, d1, e1;
     {
       // plane 0 through the LSU (256-bit), plane 1 through the texture path:
@@ -641,6 +643,7 @@ __global__ void __launch_bounds__(K2T, TAC_K2_MINB) band_shade_kernel(const __gr
     const bool act = y < H && (!PAD || xg < W);  // xg >= W: row padding, idle
     if (__all_sync(0xffffffffu, !act)) break;  // uniform per warp
     const int yc = act ? y : H - 1;
+    TAC_CHECK(yc >= 0 && yc < H && (xg + 4 <= W || (PAD && !act)));
     const float* rc = img + (long long)yc * W;
     // columns whose gradient can be non-zero: band extents of rows y-1..y+1
     // (union over the blur kernel's column strips), +-1

@@ -6,6 +6,22 @@
 
 #include "../../include/tac_b200.h"
 
+// Debug bounds checks (build with -DTAC_DEBUG_CHECKS: `make CHECKS=1` ->
+// libtac_b200_checks.so): a failed index check traps the kernel, so the call
+// returns a CUDA error and the test fails.  compute-sanitizer is closed on the
+// GPU pool; this build runs the GPU suite with every shared-memory and global
+// index of the hot kernels checked.  Compiled out otherwise.
+#ifdef TAC_DEBUG_CHECKS
+#define TAC_CHECK(cond)      \
+  do {                       \
+    if (!(cond)) __trap();   \
+  } while (0)
+#else
+#define TAC_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace tac {
 
 // Strip-streaming frame kernel geometry (see tac_frame.cu).

@@ -136,6 +136,7 @@ __device__ inline void markers_block(const MarkerGeom& g, const Load& l, float* 
     const int y = s_rows[m] + dy;
     const int x = s_cols[m] + dx;
     if (y < 0 || y >= g.H || x < 0 || x >= g.W) continue;
+    TAC_CHECK(y >= 0 && y < g.H && x >= 0 && x < g.W);
     uint8_t* px = rgb + ((long long)y * g.W + x) * 3;
     px[0] = g.dot_r;
     px[1] = g.dot_g;

@@ -171,6 +171,11 @@ __global__ void __launch_bounds__(kTileThreads, 3) shadow_tiled_kernel(
     for (; st + 1 < s.steps; st += 2) {
       const char* b0 = base + offb[st];
       const char* b1 = base + offb[st + 1];
+      TAC_CHECK(b0 >= reinterpret_cast<const char*>(reg) && b1 >= reinterpret_cast<const char*>(reg) &&
+                b0 + ((RPW - 1) * rw + 32 * (CPL - 1) + 1) * (int)sizeof(float) <=
+                    reinterpret_cast<const char*>(reg + rh * rw) &&
+                b1 + ((RPW - 1) * rw + 32 * (CPL - 1) + 1) * (int)sizeof(float) <=
+                    reinterpret_cast<const char*>(reg + rh * rw));
       const float2 cs = make_float2(-sg * cost[st], -sg * cost[st + 1]);  // a = x - sg c
 #pragma unroll
       for (int r = 0; r < RPW; ++r)

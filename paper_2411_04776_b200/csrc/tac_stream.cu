@@ -158,6 +158,8 @@ __device__ __forceinline__ bool h_item(const FrameParams& p, const float* vs, co
     float2 v[8 + 2 * PY::R4];
 #pragma unroll
     for (int q = 0; q < (8 + 2 * r4l) / 2; ++q) {
+      TAC_CHECK(2 * (c0 - vx0) + 2 * (R4 - r4l) + 4 * q >= 0 &&
+                2 * (c0 - vx0) + 2 * (R4 - r4l) + 4 * q + 4 <= G::RPP);
       const float4 f = *reinterpret_cast<const float4*>(base + l * (SB / 2) * G::RPP + 2 * (R4 - r4l) + 4 * q);
       v[2 * q] = make_float2(f.x, f.y);
       v[2 * q + 1] = make_float2(f.z, f.w);
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
     // read + convert one row y from smem slot / row; rows < H are folded into
     // the contact partials (rows >= H are replicas of row H-1)
     auto take = [&](int y, const float* src_row) -> float2 {
+      TAC_CHECK(src_row >= in_s && src_row + 2 <= in_s + NS * SB * G::IP && (cr - vx0) + 2 <= G::IP);
       const float2 raw = *reinterpret_cast<const float2*>(src_row);
       float2 v = raw;
       if (depth_in) {
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
 #pragma unroll
         for (int l = 0; l < L; ++l) {
           // rows (2k, 2k+1) x columns (c, c+1)
+          TAC_CHECK(!act || (2 * (c - vx0 + R4) >= 0 && 2 * (c - vx0 + R4) + 4 <= G::RPP));
           if (act)
             *reinterpret_cast<float4*>(vs + (l * (SB / 2) + k) * G::RPP) =
                 make_float4(oa[l].x, ob[l].x, oa[l].y, ob[l].y);
@@ -449,9 +453,11 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
               const int k = i / (2 * np), rem = i - k * 2 * np, side = rem >= np ? 1 : 0, t = rem - side * np;
               float* lrow = vblk + (l * (SB / 2) + k) * G::RPP;
               if (side == 0 && vx0 == 0) {
+                TAC_CHECK(2 * (R4 - 2 * np + 2 * t) >= 0);
                 const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * R4);
                 *reinterpret_cast<float4*>(lrow + 2 * (R4 - 2 * np + 2 * t)) = make_float4(e.x, e.y, e.x, e.y);
               } else if (side == 1 && vx1 == W) {
+                TAC_CHECK(2 * (W - vx0 + R4 + 2 * t) + 4 <= G::RPP);
                 const float2 e = *reinterpret_cast<const float2*>(lrow + 2 * (W - 1 - vx0 + R4));
                 *reinterpret_cast<float4*>(lrow + 2 * (W - vx0 + R4 + 2 * t)) = make_float4(e.x, e.y, e.x, e.y);
               }
@@ -468,7 +474,8 @@ __global__ void __launch_bounds__(PY::MAXT, PY::MINB) stream_blur_kernel(const _
         float2 acc[8];
         h_item<PY, G>(p, vs, s_nz + (sv * (SB / 2) + m) * kMaxVW, m, c0, vx0, item == ht ? hw0 : hw1, acc);
         const int y = SB * j + 2 * m;
-        float* d = p.scratch + env * HW + (long long)y * W + c0;
+        TAC_CHECK(c0 >= 0 && c0 + 8 <= W && m >= 0 && m < SB / 2);
+      float* d = p.scratch + env * HW + (long long)y * W + c0;
         if (y < H) {
           reinterpret_cast<float4*>(d)[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
           reinterpret_cast<float4*>(d)[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);

@@ -12,7 +12,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 from _helpers import depth_batch, small_config  # noqa: E402
-from paper_2411_04776_b200 import TactilePipeline, render_heightmaps, synthetic  # noqa: E402
+from paper_2411_04776_b200 import (DEFAULT_PYRAMID, TactilePipeline, levels_from_kernel_sizes,  # noqa: E402
+                                   render_heightmaps, synthetic)
 
 import dataclasses  # noqa: E402
 
@@ -21,7 +22,11 @@ cases = [(synthetic.baseline_config(2, 0)[0], 3),            # stream blur, sigm
          (small_config(37, 480, grid=(3, 5)), 2),             # column strips, padded shade rows
          (small_config(48, 64, shadows=True), 2),             # tiled shadow march, stream path
          (dataclasses.replace(small_config(48, 64), lut_dtype="f16"), 2),
-         (small_config(40, 56, shadows=True), 2)]             # L1 shadow march + fused-path fallback
+         (small_config(40, 56, shadows=True), 2),             # L1 shadow march + fused-path fallback
+         (synthetic.baseline_config(3, 0)[0], 2),            # 480x640 sigma 1,2,4,8: wide strips, R4 = 24
+         (small_config(50, 640, grid=(4, 6),                  # REF DEFAULT_PYRAMID, strips, ragged rows
+                       levels=levels_from_kernel_sizes(DEFAULT_PYRAMID)), 2),
+         (dataclasses.replace(small_config(48, 64), kernel_path="band"), 2)]  # band blur kernel
 for cfg, n in cases:
     h, w = cfg.sensor.image_size
     pipe = TactilePipeline(cfg, "cuda")
