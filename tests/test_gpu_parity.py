@@ -898,6 +898,51 @@ class TestParityAtScale:
             assert obs.summary[i, 0].item() == ref["summary"][0]
         assert worst >= RGB_FRAC
 
+    def test_full_32768_env_configs4_launch(self):
+        """configs[4] at its full size, as bench.py times it (one tac_pipeline
+        call over all 32768 envs, one blur/shade launch pair).  Properties
+        that hold at any size: (1) every env's contact flag and contact area
+        equal the fp64 count of indentation > threshold (REF/marker.py:109-121)
+        over its own map, for all 32768 envs; (2) envs re-run as a small batch
+        give bit-identical RGB, displacements and summaries wherever they sat
+        in the big launch (no dependence on batch position, chunking or the
+        grid); (3) a sample of them matches the oracle."""
+        cfg, n, params, shear, twist = synthetic.workload(4, 0)
+        assert n == 32768
+        h, w = cfg.sensor.image_size
+        depth = synthetic.height_maps(params, h, w, device=DEV, dtype=torch.float32, chunk=1024)
+        pipe = TactilePipeline(cfg, DEV)
+        sh = torch.as_tensor(shear, dtype=torch.float64, device=DEV)
+        tw = torch.as_tensor(twist, dtype=torch.float64, device=DEV)
+        obs = pipe.simulate(depth, sh, tw)
+        torch.cuda.synchronize()
+        # (1) contact flag / area of every env against an fp64 count
+        rest, thr, pitch = cfg.sensor.gelpad_thickness, cfg.contact_threshold, cfg.pixel_pitch
+        count = torch.empty(n, dtype=torch.float64, device=DEV)
+        for e0 in range(0, n, 2048):
+            ind = (rest - depth[e0:e0 + 2048].double()).clamp(0.0, rest)
+            count[e0:e0 + 2048] = (ind > thr).sum(dim=(1, 2)).double()
+        summ = obs.summary.double()
+        assert torch.equal(summ[:, 0], (count > 0).double())
+        area = count * pitch * pitch
+        assert torch.allclose(summ[:, 1], area.float().double(), rtol=1e-6, atol=0.0)
+        assert 0.2 < float((count > 0).double().mean()) < 1.0
+        # (2) batch-position independence, incl. the first / last envs
+        pick = np.unique(np.concatenate([[0, 1, n // 2 - 1, n // 2, n - 2, n - 1],
+                                         np.random.default_rng(11).choice(n, 42, replace=False)]))
+        idx = torch.as_tensor(pick, device=DEV)
+        small = pipe.simulate(depth[idx].contiguous(), sh[idx].contiguous(), tw[idx].contiguous())
+        torch.cuda.synchronize()
+        assert torch.equal(small.rgb, obs.rgb[idx])
+        assert torch.equal(small.disp, obs.disp[idx])
+        assert torch.equal(small.summary, obs.summary[idx])
+        # (3) oracle on 8 of them
+        for k in pick[:: max(1, len(pick) // 8)][:8]:
+            ref = oracle_env(cfg, depth[k].cpu().numpy(), shear[k], twist[k])
+            _, frac = rgb_stats(obs.rgb[k].cpu().numpy(), ref["rgb"])
+            assert frac >= RGB_FRAC
+            assert normwise(obs.disp[k].cpu().numpy(), ref["disp"]) <= DISP_TOL
+
     @pytest.mark.parametrize("pyramid", ["sigma1248", "default"])
     def test_16_envs_480x640(self, pyramid):
         cfg, _ = synthetic.baseline_config(3)
