@@ -745,6 +745,35 @@ class TestBandPathShapes:
         assert torch.equal(got.disp, ref.disp.cpu())
         assert torch.equal(got.summary, ref.summary.cpu())
 
+    @pytest.mark.parametrize("path", ["stream", "fused"])
+    def test_host_streamer_multi_strip_ragged_chunks(self, path):
+        """Multi-strip frames (W=480: two column strips, per-env arrival
+        counters in the workspace) through ragged host chunks (4,4,3 on two
+        alternating streams) and a shrinking batch on one stream: the counters
+        of a smaller call must not land on stale partials of a larger one
+        (tac_abi.cu plan_workspace)."""
+        from paper_2411_04776_b200.hostio import simulate_host
+
+        cfg = dataclasses.replace(small_config(40, 480, grid=(3, 5)), kernel_path=path)
+        n = 11
+        depth = depth_batch(n, 40, 480, seed=71)
+        shear, twist = synthetic.loads(n, 72)
+        pipe = TactilePipeline(cfg, DEV)
+        sh = torch.as_tensor(shear, dtype=torch.float64)
+        tw = torch.as_tensor(twist, dtype=torch.float64)
+        ref = pipe.simulate(depth.to(DEV), sh.to(DEV), tw.to(DEV))
+        torch.cuda.synchronize()
+        got = simulate_host(pipe, depth.pin_memory(), sh.pin_memory(), tw.pin_memory(), chunk=4)
+        assert torch.equal(got.rgb, ref.rgb.cpu())
+        assert torch.equal(got.disp, ref.disp.cpu())
+        assert torch.equal(got.summary, ref.summary.cpu())
+        # shrinking batch on the current stream, same workspace
+        for m in (7, 3, 1):
+            part = pipe.simulate(depth[:m].to(DEV), sh[:m].to(DEV), tw[:m].to(DEV))
+            assert torch.equal(part.rgb, ref.rgb[:m])
+            assert torch.equal(part.disp, ref.disp[:m])
+            assert torch.equal(part.summary, ref.summary[:m])
+
 class TestDiagnostics:
     def test_launch_count_and_profile(self):
         cfg = small_config(48, 64)
