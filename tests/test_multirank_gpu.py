@@ -84,3 +84,70 @@ def test_two_ranks_equal_one_full_batch():
         assert np.array_equal(rgb, ref.rgb[s:e].cpu().numpy())
         assert np.array_equal(disp, ref.disp[s:e].cpu().numpy())
     assert ref.summary[:, 0].sum() > 0  # the batch has contacts
+
+
+def _nccl_worker(port, q):
+    """bench.py's N>1 step loop on a one-rank NCCL communicator: the pipeline
+    on the main stream, the [blk, 8] summary all-gather (device tensors,
+    ``all_gather_into_tensor``) on a side stream, summaries double-buffered."""
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        from paper_2411_04776_b200 import TactilePipeline, synthetic
+        from paper_2411_04776_b200.sharding import gather_summaries
+
+        cfg, n, params, shear, twist = synthetic.workload(2, 5, n_total=N_TOTAL)
+        depth = synthetic.height_maps(params, 240, 320, device=dev, dtype=torch.float32)
+        sh, tw = torch.as_tensor(shear, device=dev), torch.as_tensor(twist, device=dev)
+        pipe = TactilePipeline(cfg, dev)
+        ref = pipe.simulate(depth, sh, tw).summary.clone()
+        blk = n + 3  # padded block, as a ragged split pads to ceil(n_total / world)
+        gathered = torch.full((blk, 8), -1.0, dtype=torch.float32, device=dev)
+        summ = [torch.zeros((blk, 8), dtype=torch.float32, device=dev) for _ in range(2)]
+        outs = [pipe.allocate(n), pipe.allocate(n)]
+        for k in range(2):
+            outs[k].summary = summ[k][:n]
+        args = [pipe.launch_args(depth, sh, tw, outs[k]) for k in range(2)]
+        side = torch.cuda.Stream(dev)
+        main = torch.cuda.current_stream(dev)
+        done = [torch.cuda.Event(), torch.cuda.Event()]
+        freed = [torch.cuda.Event(), torch.cuda.Event()]
+        for step in range(5):
+            k = step & 1
+            if step >= 2:
+                main.wait_event(freed[k])
+            pipe.launch(args[k])
+            done[k].record(main)
+            side.wait_event(done[k])
+            with torch.cuda.stream(side):
+                gather_summaries(summ[k], gathered)
+                freed[k].record(side)
+        main.wait_stream(side)
+        torch.cuda.synchronize()
+        q.put((dist.get_backend(), gathered[:n].cpu().numpy(), ref.cpu().numpy(), gathered[n:].cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_summary_all_gather_on_a_side_stream():
+    """The NCCL leg of bench.py --gpus N (all_gather_into_tensor of the
+    per-env summaries on a side stream, double-buffered against the next
+    step's kernels) on a one-rank communicator: this run has one GPU, so the
+    collective's N>1 exchange itself stays unmeasured."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    backend, got, ref, pad = q.get(timeout=300)
+    p.join(60)
+    assert p.exitcode == 0
+    assert backend == "nccl"
+    assert np.array_equal(got, ref)
+    assert not pad.any()
